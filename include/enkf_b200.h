@@ -1,0 +1,135 @@
+/*
+ * enkf_b200.h — C ABI of the B200-native EnKF analysis step
+ * (iterative Sherman-Morrison, arXiv 1302.3876).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point names the
+ * reference interface it replaces (files under /root/reference/pkg/src/enkfkit,
+ * read-only, not shipped):
+ *
+ *   enkf_analysis_f64       enkf.py:167-192   analysis_step(x, obs, h, r, "sherman")
+ *                                              (unlocalized branch, workers ignored)
+ *   enkf_analysis_host_f64  same, host buffers (copies in/out inside the call)
+ *   enkf_ism_solve_f64      sherman.py:253-286 solve_sherman(r, v, d) -> SolverResult.z
+ *   enkf_ism_gram_f64       sherman.py:149-205 level 0 + the per-level dots v_k'u (K4/K5/K8),
+ *                           fused into one Gram pass; the multi-GPU split point
+ *   enkf_ism_levels_f64     sherman.py:164-187 the N Sherman-Morrison levels (den_k, singular
+ *                           guard, composition), run on the reduced N x 2N Gram
+ *   enkf_anomaly_update_f64 enkf.py:192        x + s @ A  (A = v' z), as X @ T
+ *   enkf_member_deviations_f64 enkf.py:82-92   member_deviations
+ *   enkf_innovations_f64    enkf.py:114-120    innovations (Y - H X)
+ *
+ * Layouts (all fp64 row-major, the reference's C-order arrays):
+ *   X, XA : [n_state][n_ens]      Y, D, V, Z : [n_obs][n_ens]
+ *   idx   : int64 [n_obs], strictly increasing, or NULL for the identity H
+ *   r     : [n_obs] observation-error variances (> 0)
+ *   gram  : [n_ens][2 n_ens]      A, T : [n_ens][n_ens]
+ * Device pointers unless the name says _host.  Stream = cudaStream_t as void*.
+ *
+ * Status codes map 1:1 onto the reference's exceptions (errors.py, enkf.py):
+ *   ENKF_OK                 -> (return value)
+ *   ENKF_INVALID_ARGUMENT   -> ValueError        (sherman.py:85-108, enkf.py:185-186)
+ *   ENKF_INDEX_RANGE        -> IndexError        (enkf.py:54-58)
+ *   ENKF_SINGULAR_UPDATE    -> SingularUpdateError(level, denominator) (sherman.py:171-174)
+ *   ENKF_NOT_SUPPORTED      -> NotImplementedError (shape outside the kernels' range)
+ *   ENKF_CUDA_ERROR         -> RuntimeError
+ */
+#ifndef ENKF_B200_H
+#define ENKF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum enkf_code {
+  ENKF_OK = 0,
+  ENKF_INVALID_ARGUMENT = 1,
+  ENKF_INDEX_RANGE = 2,
+  ENKF_SINGULAR_UPDATE = 3,
+  ENKF_NOT_SUPPORTED = 4,
+  ENKF_CUDA_ERROR = 5
+};
+
+typedef struct enkf_status {
+  int32_t code;        /* enum enkf_code */
+  int32_t level;       /* 1-based Sherman-Morrison level for ENKF_SINGULAR_UPDATE */
+  double denominator;  /* 1 + v_k' u_k at that level */
+  char message[256];
+} enkf_status;
+
+typedef struct enkf_plan enkf_plan;
+
+/* Library identification: "enkf_b200 <version> sm_100a". */
+const char* enkf_version(void);
+/* Largest ensemble size the kernels accept (the N x 2N Gram recursion runs in
+ * one CTA's shared memory). */
+int32_t enkf_max_ens(void);
+
+/* Select the CUDA device for subsequent plan creation / helper calls on this
+ * host thread (the library links its own CUDA runtime; callers that manage
+ * devices elsewhere, e.g. torch, pass their device index here). */
+int32_t enkf_set_device(int32_t device);
+
+/* Plan: owns the device workspace (Gram partials, Gram, A, T, status) for one
+ * (n_state, n_obs, n_ens) shape on the current device.  No allocation happens
+ * in the compute calls.  Thread-safe per plan (one call at a time). */
+int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens,
+                         enkf_plan** plan, enkf_status* status);
+void enkf_plan_destroy(enkf_plan* plan);
+
+/* Full analysis step on device buffers (single GPU or one shard whose obs rows
+ * are all local).  XA may equal X (in-place update).  Synchronous: returns
+ * after the stream is drained and the status is read. */
+int32_t enkf_analysis_f64(enkf_plan* plan, const double* X, const double* Y,
+                          const int64_t* idx, const double* r, double* XA,
+                          void* stream, enkf_status* status);
+
+/* Same, without the final synchronisation: the status stays on the device
+ * until enkf_plan_sync_status().  Graph-capturable. */
+int32_t enkf_analysis_async_f64(enkf_plan* plan, const double* X, const double* Y,
+                                const int64_t* idx, const double* r, double* XA,
+                                void* stream);
+int32_t enkf_plan_sync_status(enkf_plan* plan, void* stream, enkf_status* status);
+/* Clear the device status word (start of a staged step). */
+int32_t enkf_plan_reset_status(enkf_plan* plan, void* stream);
+
+/* Full analysis step on HOST buffers: copies X, Y, idx, r in, runs the step,
+ * copies XA out.  Pinned host memory is used at full PCIe speed. */
+int32_t enkf_analysis_host_f64(enkf_plan* plan, const double* X_h, const double* Y_h,
+                               const int64_t* idx_h, const double* r_h, double* XA_h,
+                               enkf_status* status);
+
+/* --- staged form (multi-GPU: partial Gram -> allreduce by the caller -> levels) --- */
+
+/* Level 0 + Gram over this plan's obs rows: gram = [V'R^-1 V | V'R^-1 D]
+ * (n_ens x 2 n_ens), V = H S, D = Y - H X, S = (X - mean)/sqrt(N-1).
+ * Input checks (non-finite, r <= 0, idx order/range) are flagged on the device. */
+int32_t enkf_ism_gram_f64(enkf_plan* plan, const double* X, const double* Y,
+                          const int64_t* idx, const double* r, double* gram,
+                          void* stream);
+/* The N Sherman-Morrison levels on a (globally reduced) Gram.  Writes
+ * A = V'Z (n_ens x n_ens), the anomaly transform T = I + (I - 11'/N) A/sqrt(N-1),
+ * and den[k] = 1 + v_k'u_k (n_ens) when den != NULL. */
+int32_t enkf_ism_levels_f64(enkf_plan* plan, const double* gram, double* A, double* T,
+                            double* den, void* stream);
+/* XA[rows] = X[rows] @ T  ==  X + S (V'Z).  XA may equal X. */
+int32_t enkf_anomaly_update_f64(enkf_plan* plan, const double* X, const double* T,
+                                double* XA, int64_t n_rows, void* stream);
+
+/* --- solve_sherman parity (sherman.py:253-286): Z = (R + V V')^-1 D --- */
+int32_t enkf_ism_solve_f64(enkf_plan* plan, const double* r, const double* V,
+                           const double* D, double* Z, double* A, void* stream,
+                           enkf_status* status);
+
+/* --- row-local helpers of the path --- */
+int32_t enkf_member_deviations_f64(const double* X, double* S, int64_t n_rows,
+                                   int64_t n_ens, void* stream);
+int32_t enkf_innovations_f64(const double* X, const double* Y, const int64_t* idx,
+                             double* D, int64_t n_obs, int64_t n_ens, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ENKF_B200_H */

@@ -1,0 +1,58 @@
+"""B200-native EnKF analysis step (iterative Sherman-Morrison, arXiv 1302.3876).
+
+Drop-in for the hot path of the reference package `enkfkit`: the names below
+keep the reference's signatures and semantics (reference __init__.py:11-84),
+while the arithmetic runs in hand-written sm_100a CUDA (libenkf_b200.so,
+C ABI in include/enkf_b200.h).  Out-of-scope reference components (models,
+twin-experiment harness, Cholesky/SVD baselines, localization, CLI) are not
+provided.
+"""
+
+from .enkf import (
+    ObservationBatch,
+    SelectionOperator,
+    analysis_step,
+    innovations,
+    member_deviations,
+)
+from .errors import (
+    ConfigError,
+    DivergenceError,
+    NotPositiveDefiniteError,
+    NumericalFailureError,
+    SingularUpdateError,
+)
+from .sherman import (
+    GROUP_LEVELS,
+    SINGULAR_TOL,
+    SolverResult,
+    level_blocks,
+    long_op_count,
+    solve_sherman,
+    solve_sherman_blocked,
+)
+from .solvers import SolverChoice, solve_analysis
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ConfigError",
+    "DivergenceError",
+    "GROUP_LEVELS",
+    "NotPositiveDefiniteError",
+    "NumericalFailureError",
+    "ObservationBatch",
+    "SINGULAR_TOL",
+    "SelectionOperator",
+    "SingularUpdateError",
+    "SolverChoice",
+    "SolverResult",
+    "analysis_step",
+    "innovations",
+    "level_blocks",
+    "long_op_count",
+    "member_deviations",
+    "solve_analysis",
+    "solve_sherman",
+    "solve_sherman_blocked",
+]

@@ -1,0 +1,250 @@
+"""Filter-core drop-in: `analysis_step` and its data types on the B200 path.
+
+Mirrors `enkfkit.enkf` (reference enkf.py) for the names on the hot path:
+`SelectionOperator`, `ObservationBatch`, `member_deviations`, `innovations`,
+`analysis_step`.  Same signatures, argument meaning, array layout (Nstate x
+Nens, C order) and error behaviour; the arithmetic runs in libenkf_b200.so
+(sm_100a) and nothing falls back to the CPU.
+
+Array types: numpy (or array-like) inputs take the host path — one C-ABI call
+that copies in, runs the step and copies out — and return numpy arrays.
+`torch.Tensor` inputs on a CUDA device stay device-resident and return a
+CUDA tensor.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .solvers import SolverChoice, _require_sherman
+
+try:  # torch is the device-memory / stream plumbing
+    import torch
+except ImportError:  # pragma: no cover - torch is part of the image
+    torch = None
+
+
+def _is_cuda_tensor(a) -> bool:
+    return torch is not None and isinstance(a, torch.Tensor) and a.is_cuda
+
+
+def _cuda_ready(device_index: int | None = None) -> int:
+    if torch is None or not torch.cuda.is_available():
+        raise RuntimeError("the EnKF analysis path needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    if device_index is None:
+        device_index = torch.cuda.current_device()
+    return int(device_index)
+
+
+@dataclass(frozen=True)
+class SelectionOperator:
+    """Observation operator selecting state rows by index (enkf.py:22-59).
+
+    ``indices`` strictly increasing and non-negative (validated at
+    construction), or ``None`` for the identity.  A device copy of the index
+    array is cached per CUDA device on first use.
+    """
+
+    indices: np.ndarray | None
+    _device_cache: dict = field(default_factory=dict, compare=False, repr=False)
+
+    @classmethod
+    def identity(cls) -> "SelectionOperator":
+        return cls(indices=None)
+
+    @classmethod
+    def from_indices(cls, indices) -> "SelectionOperator":
+        if _is_cuda_tensor(indices):
+            indices = indices.cpu().numpy()
+        idx = np.asarray(indices, dtype=np.intp)
+        if idx.ndim != 1 or idx.size < 1:
+            raise ValueError("need a non-empty 1-D index array")
+        if np.any(np.diff(idx) <= 0):
+            raise ValueError("indices must be strictly increasing")
+        if idx[0] < 0:
+            raise ValueError("indices must be non-negative")
+        return cls(indices=np.ascontiguousarray(idx, dtype=np.int64))
+
+    def nobs(self, nstate: int) -> int:
+        return nstate if self.indices is None else int(self.indices.size)
+
+    def check_range(self, nstate: int) -> None:
+        """The IndexError of enkf.py:54-58."""
+        if self.indices is not None and self.indices[-1] >= nstate:
+            raise IndexError(f"observation index {self.indices[-1]} out of range "
+                             f"for state size {nstate}")
+
+    def device_indices(self, device):
+        if self.indices is None:
+            return None
+        key = str(device)
+        t = self._device_cache.get(key)
+        if t is None:
+            t = torch.from_numpy(np.ascontiguousarray(self.indices, dtype=np.int64)).to(device)
+            self._device_cache[key] = t
+        return t
+
+    def apply(self, x):
+        """Select observed rows (identity returns ``x`` itself, enkf.py:50-59)."""
+        if self.indices is None:
+            return x
+        self.check_range(x.shape[0])
+        if _is_cuda_tensor(x):
+            return x.index_select(0, self.device_indices(x.device))
+        return x[self.indices]
+
+
+@dataclass(frozen=True)
+class ObservationBatch:
+    """One observation vector and its per-member perturbed copies
+    (enkf.py:62-71): ``perturbed[:, j] == y + perturbations[:, j]``."""
+
+    y: object
+    perturbed: object
+    perturbations: object
+
+
+def _f64_contig_device(a, device):
+    if _is_cuda_tensor(a):
+        t = a
+        if t.device != device:
+            t = t.to(device)
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))).to(device)
+    if t.dtype != torch.float64:
+        t = t.to(torch.float64)
+    return t.contiguous()
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def member_deviations(x):
+    """S = (X - row mean) / sqrt(N - 1) on the GPU (enkf.py:82-92)."""
+    dev_in = _is_cuda_tensor(x)
+    if not dev_in:
+        x = np.asarray(x, dtype=float)
+    if x.ndim != 2 or x.shape[1] < 2:
+        raise ValueError("need at least 2 ensemble members for deviations")
+    device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
+    xd = _f64_contig_device(x, device)
+    out = torch.empty_like(xd)
+    _native.lib().enkf_set_device(device.index)
+    code = _native.lib().enkf_member_deviations_f64(
+        xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1], _stream_ptr(device))
+    _native.raise_for_status(code, None, "enkf_member_deviations_f64")
+    return out if dev_in else out.cpu().numpy()
+
+
+def innovations(obs: ObservationBatch, h: SelectionOperator, x):
+    """D = Y - H(X) on the GPU (enkf.py:114-120)."""
+    dev_in = _is_cuda_tensor(x)
+    if not dev_in:
+        x = np.asarray(x, dtype=float)
+    h.check_range(x.shape[0])
+    device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
+    xd = _f64_contig_device(x, device)
+    yd = _f64_contig_device(obs.perturbed, device)
+    nobs = h.nobs(xd.shape[0])
+    if yd.dim() != 2 or yd.shape[0] != nobs or (xd.dim() == 2 and yd.shape[1] != xd.shape[1]):
+        raise ValueError(f"perturbed observations {tuple(yd.shape)} do not match "
+                         f"H(x) ({nobs}, {xd.shape[1] if xd.dim() == 2 else 1})")
+    out = torch.empty_like(yd)
+    idx = h.device_indices(device)
+    _native.lib().enkf_set_device(device.index)
+    code = _native.lib().enkf_innovations_f64(
+        xd.data_ptr(), yd.data_ptr(), 0 if idx is None else idx.data_ptr(),
+        out.data_ptr(), nobs, yd.shape[1], _stream_ptr(device))
+    _native.raise_for_status(code, None, "enkf_innovations_f64")
+    return out if dev_in else out.cpu().numpy()
+
+
+def _check_obs_shapes(nobs: int, nens: int, perturbed_shape, r_shape):
+    if len(perturbed_shape) != 2 or tuple(perturbed_shape) != (nobs, nens):
+        raise ValueError(f"perturbed observations have shape {tuple(perturbed_shape)}, "
+                         f"expected ({nobs}, {nens})")
+    if len(r_shape) != 1:
+        raise ValueError(f"r must be a vector, got shape {tuple(r_shape)}")
+    if r_shape[0] != nobs:
+        raise ValueError(f"row mismatch: r has {r_shape[0]}, V has {nobs}, D has {nobs}")
+
+
+def analysis_step(
+    x,
+    obs: ObservationBatch,
+    h: SelectionOperator,
+    r,
+    solver: SolverChoice | str = SolverChoice.SHERMAN,
+    localization=None,
+    workers: int = 1,
+):
+    """One stochastic-EnKF analysis update, X^A = X + S (V'Z) (enkf.py:167-192).
+
+    Same signature as the reference.  ``solver`` must be "sherman" (the other
+    reference solvers are not on this path); ``localization`` is not
+    supported (the dense Nstate x Nobs influence matrix is out of scope);
+    ``workers`` is accepted and ignored (the GPU result does not depend on it).
+    Returns a new array; inputs are never modified.
+    """
+    _require_sherman(solver)
+    if localization is not None:
+        raise NotImplementedError("localized analysis (enkf.py:193-199) is not on the B200 path")
+    dev_in = _is_cuda_tensor(x)
+    if not dev_in:
+        x = np.asarray(x, dtype=float)
+    if x.ndim != 2 or x.shape[1] < 2:
+        raise ValueError("analysis needs at least 2 ensemble members")
+    nstate, nens = int(x.shape[0]), int(x.shape[1])
+    if nens > _native.max_ens():
+        raise NotImplementedError(f"n_ens={nens} exceeds the supported maximum {_native.max_ens()}")
+    h.check_range(nstate)
+    nobs = h.nobs(nstate)
+    perturbed = obs.perturbed
+    if not _is_cuda_tensor(perturbed):
+        perturbed = np.asarray(perturbed, dtype=float)
+    r_host = r.detach().cpu().numpy() if _is_cuda_tensor(r) else np.asarray(r, dtype=float)
+    _check_obs_shapes(nobs, nens, tuple(perturbed.shape), r_host.shape)
+    if np.any(r_host <= 0):
+        raise ValueError("observation variances must be positive")
+    if not np.all(np.isfinite(r_host)):
+        raise ValueError("inputs contain non-finite entries")
+
+    if dev_in:
+        device = x.device
+        _cuda_ready(device.index)
+        plan = _native.get_plan(device.index, nstate, nobs, nens)
+        xd = _f64_contig_device(x, device)
+        yd = _f64_contig_device(perturbed, device)
+        rd = _f64_contig_device(r, device)
+        idx = h.device_indices(device)
+        out = torch.empty_like(xd)
+        st = _native.EnkfStatus()
+        with plan.lock:
+            code = _native.lib().enkf_analysis_f64(
+                plan.handle, xd.data_ptr(), yd.data_ptr(),
+                0 if idx is None else idx.data_ptr(), rd.data_ptr(), out.data_ptr(),
+                _stream_ptr(device), ctypes.byref(st))
+        _native.raise_for_status(code, st, "enkf_analysis_f64")
+        return out
+
+    device_index = _cuda_ready()
+    plan = _native.get_plan(device_index, nstate, nobs, nens)
+    xh = np.ascontiguousarray(x, dtype=np.float64)
+    yh = np.ascontiguousarray(perturbed, dtype=np.float64)
+    rh = np.ascontiguousarray(r_host, dtype=np.float64)
+    idxh = None if h.indices is None else np.ascontiguousarray(h.indices, dtype=np.int64)
+    out = np.empty_like(xh)
+    st = _native.EnkfStatus()
+    with plan.lock:
+        code = _native.lib().enkf_analysis_host_f64(
+            plan.handle, xh.ctypes.data, yh.ctypes.data,
+            None if idxh is None else idxh.ctypes.data, rh.ctypes.data, out.ctypes.data,
+            ctypes.byref(st))
+    _native.raise_for_status(code, st, "enkf_analysis_host_f64")
+    return out

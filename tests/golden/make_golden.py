@@ -1,0 +1,162 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the reference is importable only there):
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+It imports `enkfkit` from /root/reference/pkg/src (read-only) and writes
+small .npz files next to this script.  The GPU box never reads the reference;
+tests compare the oracle restatement (CPU tests) and the CUDA path (GPU tests)
+against these files.  Inputs are regenerated from the recorded Philox seeds
+where storing them would be large; a checksum of every regenerated input is
+stored so drift is detected.
+"""
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+sys.dont_write_bytecode = True
+
+import enkfkit  # noqa: E402  (the reference)
+from enkfkit import enkf as ref_enkf  # noqa: E402
+from enkfkit import sherman as ref_sherman  # noqa: E402
+from enkfkit.models import Lorenz96, Lorenz96Config  # noqa: E402
+from enkfkit.observations import build_selection_operator  # noqa: E402
+from enkfkit.rng import gaussian_matrix, make_rng  # noqa: E402
+
+from paper_1302_3876_b200 import workloads as W  # noqa: E402
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def ism_systems():
+    """solve_sherman on random systems: the reference tests' shapes
+    (tests/test_sherman.py:41-53, 85-94; test_acceptance.py:44-61)."""
+    out = {}
+    cases = [(31, 5, 3), (90, 50, 2), (56, 200, 16), (168, 2000, 128), (57, 150, 1),
+             (59, 150, 3), (64, 150, 8), (65, 150, 9), (72, 150, 16), (87, 150, 31)]
+    rng = make_rng(0xA1)
+    for _ in range(12):  # C1-style: Nobs log-uniform 10-500, N log-uniform 2-64
+        nobs = int(round(np.exp(rng.uniform(np.log(10), np.log(500)))))
+        nens = int(round(np.exp(rng.uniform(np.log(2), np.log(64)))))
+        cases.append((int(rng.integers(1000, 10**6)), nobs, nens))
+    for i, (seed, nobs, nens) in enumerate(cases):
+        g = make_rng(seed)
+        r = g.uniform(0.5, 2.0, nobs)
+        v = g.standard_normal((nobs, nens))
+        d = g.standard_normal((nobs, nens))
+        res = ref_sherman.solve_sherman(r, v, d)
+        zl, ops = ref_sherman._sweep_reference(r, v, d, count_ops=True, verify_frozen=False)
+        out[f"c{i}_meta"] = np.array([seed, nobs, nens, ops])
+        out[f"c{i}_z"] = res.z
+        out[f"c{i}_zlevel"] = zl
+        out[f"c{i}_inputs_sha"] = np.array(sha(np.concatenate([r, v.ravel(), d.ravel()])))
+    out["ncases"] = np.array(len(cases))
+    out["opcount"] = np.array([[n, m, ref_sherman.long_op_count(n, m)] for n, m in
+                               [(3, 3), (1, 1), (4, 10), (2, 7), (5, 40), (16, 320), (128, 1 << 20)]])
+    return out
+
+
+def analysis_small():
+    """analysis_step on the Kalman-gain oracle instances (test_acceptance.py:88-115),
+    zero spread (test_enkf.py:208-213), uninformative obs (:203-206)."""
+    out = {}
+    rng = make_rng(0xA3)
+    for i in range(20):
+        nstate = int(rng.integers(6, 21))
+        nens = int(rng.integers(3, 7))
+        nobs = int(rng.integers(2, min(nstate, 10) + 1))
+        x = rng.standard_normal((nstate, nens))
+        idx = np.sort(rng.choice(nstate, size=nobs, replace=False))
+        h = ref_enkf.SelectionOperator.from_indices(idx)
+        r = rng.uniform(0.2, 1.0, nobs)
+        y = rng.standard_normal(nobs)
+        eps = 0.2 * rng.standard_normal((nobs, nens))
+        obs = ref_enkf.ObservationBatch(y=y, perturbed=y[:, None] + eps, perturbations=eps)
+        xa = ref_enkf.analysis_step(x, obs, h, r, "sherman")
+        for k, val in dict(x=x, idx=idx, r=r, perturbed=obs.perturbed, xa=xa).items():
+            out[f"k{i}_{k}"] = val
+    out["nkalman"] = np.array(20)
+    x = np.tile(np.arange(6.0)[:, None], (1, 4))
+    h = ref_enkf.SelectionOperator.from_indices([1, 4])
+    yb = np.array([5.0, -2.0])
+    obs = ref_enkf.ObservationBatch(y=yb, perturbed=yb[:, None] + np.zeros((2, 4)), perturbations=np.zeros((2, 4)))
+    out["zero_x"], out["zero_xa"] = x, ref_enkf.analysis_step(x, obs, h, np.ones(2), "sherman")
+    return out
+
+
+def config_fixtures():
+    out = {}
+    # config 1 built with the reference's own model/observation code
+    ns, nens = 40, 20
+    s = W.SEEDS[1]
+    truth = gaussian_matrix(make_rng(s["truth"]), ns, 1, 8.0, 0.01)[:, 0]
+    model = Lorenz96(Lorenz96Config(nstate=ns, forcing=8.0, dt=0.05))
+    truth = model.advance(truth, 0.0, 1000 * 0.05)
+    x = truth[:, None] + gaussian_matrix(make_rng(s["ens"]), ns, nens, 0.0, 1.0)
+    h = build_selection_operator(ns, 0.5)
+    r = np.full(h.nobs(ns), 0.01)
+    rng = make_rng(s["obs"])
+    y = h.apply(truth) + gaussian_matrix(rng, r.size, 1, 0.0, np.sqrt(r))[:, 0]
+    obs = ref_enkf.perturb_observations(y, r, nens, rng)
+    xa = ref_enkf.analysis_step(x, obs, h, r, "sherman")
+    out.update(c1_x=x, c1_idx=h.indices, c1_r=r, c1_perturbed=obs.perturbed, c1_xa=xa)
+
+    # configs 2 (first cycle), 3 and a scaled config 4: inputs from our seeded
+    # generators (checksummed), outputs from the reference's analysis_step.
+    cyc = W.Config2Cycler()
+    p2 = cyc.cycle()
+    p3 = W.config3()
+    p4 = W.config4(8)
+    for tag, p in (("c2", p2), ("c3", p3), ("c4s8", p4)):
+        h = ref_enkf.SelectionOperator.identity() if p.indices is None else \
+            ref_enkf.SelectionOperator.from_indices(p.indices)
+        ob = ref_enkf.ObservationBatch(y=p.y, perturbed=p.perturbed, perturbations=p.perturbed - p.y[:, None])
+        xa = ref_enkf.analysis_step(p.x, ob, h, p.r, "sherman")
+        stride = max(1, p.x.shape[0] // 512)
+        out[f"{tag}_input_sha"] = np.array(sha(np.concatenate([p.x.ravel(), p.perturbed.ravel(), p.r])))
+        out[f"{tag}_stride"] = np.array(stride)
+        out[f"{tag}_xa_rows"] = xa[::stride]
+        out[f"{tag}_xa_colsum"] = xa.sum(axis=0)
+        out[f"{tag}_xa_absmax"] = np.array(np.abs(xa).max())
+    return out
+
+
+def selections():
+    """'Identical observation-index selection': the reference's
+    build_selection_operator for every config's H."""
+    out = {}
+    h1 = build_selection_operator(40, 0.5)
+    out["c1"] = h1.indices
+    h2 = build_selection_operator(4096, 1.0)
+    out["c2_identity"] = np.array(h2.indices is None)
+    for cfg in (4, 5):
+        z, s = W.SIZES[cfg], W.SEEDS[cfg]
+        h = build_selection_operator(z["ns"], z["nobs"] / z["ns"], "random", s["h"])
+        out[f"c{cfg}_sha"] = np.array(sha(h.indices.astype(np.int64)))
+        out[f"c{cfg}_head"] = h.indices[:512]
+        out[f"c{cfg}_tail"] = h.indices[-512:]
+        out[f"c{cfg}_n"] = np.array(h.indices.size)
+    for sl in (8, 6):
+        z, s = W.SIZES[4], W.SEEDS[4]
+        ns, nobs = z["ns"] >> sl, z["nobs"] >> sl
+        h = build_selection_operator(ns, nobs / ns, "random", s["h"])
+        out[f"c4s{sl}_sha"] = np.array(sha(h.indices.astype(np.int64)))
+    return out
+
+
+if __name__ == "__main__":
+    for name, fn in (("ism_systems", ism_systems), ("analysis_small", analysis_small),
+                     ("configs", config_fixtures), ("selection", selections)):
+        data = fn()
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **data)
+        print(name, os.path.getsize(path) // 1024, "KiB")
+    print("reference", enkfkit.__version__)

@@ -1,0 +1,277 @@
+"""Parity of the CUDA path (libenkf_b200.so via the drop-in API / C ABI)
+against the CPU oracle (oracle/) and the reference's golden fixtures.
+
+Tolerances (written here, per the north star): the analysis ensemble X^A
+within 1e-9 max-relative error (max|dX^A| / max|X^A_ref|, the reference's
+own normwise convention); Z of solve_sherman within 1e-11 relative (the
+reference tests' dense-solve bound is 1e-11 absolute, test_sherman.py:41-44).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from golden_io import ism_cases, kalman_cases, load, rel_err
+import paper_1302_3876_b200 as P
+from paper_1302_3876_b200 import _native
+from paper_1302_3876_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+XA_TOL = 1e-9
+Z_TOL = 1e-11
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_1302_3876_b200.build import build
+    build()
+    import torch
+    assert torch.cuda.is_available()
+
+
+def obs_of(p):
+    return P.ObservationBatch(y=p.y, perturbed=p.perturbed, perturbations=p.perturbed - p.y[:, None])
+
+
+def h_of(p):
+    return P.SelectionOperator.identity() if p.indices is None else P.SelectionOperator.from_indices(p.indices)
+
+
+# ---------------------------------------------------------------- solve_sherman
+@pytest.mark.parametrize("case", list(range(22)))
+def test_solve_matches_reference_golden(case):
+    seed, r, v, d, z_ref, zl_ref, ops = list(ism_cases())[case]
+    res = P.solve_sherman(r, v, d, count_ops=True)
+    assert isinstance(res.z, np.ndarray) and res.z.shape == z_ref.shape and res.z.flags.c_contiguous
+    assert rel_err(res.z, z_ref) <= Z_TOL
+    assert rel_err(res.z, zl_ref) <= Z_TOL
+    assert res.long_ops == ops
+    assert res.seconds > 0
+
+
+def test_zero_v_is_diagonal_solve():
+    z = P.solve_sherman(np.array([2.0, 2.0]), np.zeros((2, 1)), np.array([[4.0], [6.0]])).z
+    assert np.array_equal(z, [[2.0], [3.0]])
+
+
+def test_scalar_rank_one():
+    z = P.solve_sherman(np.array([1.0]), np.array([[1.0]]), np.array([[1.0]])).z
+    assert np.allclose(z, [[0.5]], atol=1e-15)
+
+
+def test_against_dense_solve():
+    g = np.random.Generator(np.random.Philox(31))
+    r = g.uniform(0.5, 2.0, 5)
+    v = g.standard_normal((5, 3))
+    d = g.standard_normal((5, 3))
+    z = P.solve_sherman(r, v, d).z
+    assert np.abs(z - np.linalg.solve(np.diag(r) + v @ v.T, d)).max() <= 1e-11
+
+
+@pytest.mark.parametrize("nobs,nens", [(50, 2), (200, 16), (2000, 128), (70000, 128), (333, 77)])
+def test_residual_bound(nobs, nens):
+    g = np.random.Generator(np.random.Philox(40 + nens))
+    r = g.uniform(0.5, 2.0, nobs)
+    v = g.standard_normal((nobs, nens))
+    d = g.standard_normal((nobs, nens))
+    z = P.solve_sherman(r, v, d).z
+    residual = np.abs(r[:, None] * z + v @ (v.T @ z) - d).max()
+    bound = 1e-10 * (np.abs(d).max() + np.abs(v).sum(axis=1).max() ** 2 * np.abs(z).max())
+    assert residual <= bound
+
+
+def test_validation_errors():
+    with pytest.raises(ValueError):
+        P.solve_sherman(np.array([1.0, 1.0]), np.ones((3, 2)), np.ones((3, 2)))
+    with pytest.raises(ValueError):
+        P.solve_sherman(np.array([1.0, -1.0]), np.ones((2, 2)), np.ones((2, 2)))
+    with pytest.raises(ValueError):
+        P.solve_sherman(np.array([1.0, 1.0]), np.ones((2, 2)), np.ones((2, 3)))
+    bad = np.ones((2, 2))
+    bad[0, 0] = np.inf
+    with pytest.raises(ValueError):
+        P.solve_sherman(np.array([1.0, 1.0]), bad, np.ones((2, 2)))
+
+
+def test_device_flags_non_finite_and_nonpositive():
+    import torch
+    dev = torch.device("cuda", 0)
+    v = torch.ones((4, 2), dtype=torch.float64, device=dev)
+    d = torch.ones((4, 2), dtype=torch.float64, device=dev)
+    d[2, 1] = float("nan")
+    with pytest.raises(ValueError):
+        P.solve_sherman(torch.ones(4, dtype=torch.float64, device=dev), v, d)
+    with pytest.raises(ValueError):
+        P.solve_sherman(torch.tensor([1.0, 1.0, 0.0, 1.0], dtype=torch.float64, device=dev), v, torch.ones_like(v))
+
+
+def _levels_on(gram_host, n):
+    import torch
+    dev = torch.device("cuda", 0)
+    plan = _native.Plan(0, 4, n, 0)
+    lib = _native.lib()
+    g = torch.as_tensor(gram_host, dtype=torch.float64, device=dev).contiguous()
+    a = torch.empty((n, n), dtype=torch.float64, device=dev)
+    den = torch.empty(n, dtype=torch.float64, device=dev)
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.enkf_plan_reset_status(plan.handle, s) == 0
+    assert lib.enkf_ism_levels_f64(plan.handle, g.data_ptr(), a.data_ptr(), None, den.data_ptr(), s) == 0
+    st = _native.EnkfStatus()
+    code = lib.enkf_plan_sync_status(plan.handle, s, ctypes.byref(st))
+    return code, st, a.cpu().numpy(), den.cpu().numpy()
+
+
+def test_singular_update_guard_reports_level():
+    # the unvalidated core (test_sherman.py:67-77): r = -1, v = d = 1 gives
+    # den_1 = 1 + v'u = 1 + 1/(-1) = 0 at level 1
+    code, st, _, _ = _levels_on(np.array([[-1.0, -1.0]]), 1)
+    assert code == _native.ENKF_SINGULAR_UPDATE and st.level == 1 and abs(st.denominator) < 1e-14
+    with pytest.raises(P.SingularUpdateError) as info:
+        _native.raise_for_status(code, st)
+    assert info.value.level == 1
+    g = np.zeros((3, 6))
+    g[0, 0], g[1, 1], g[2, 2] = 0.5, 2.0, -1.0
+    code, st, _, den = _levels_on(g, 3)
+    assert code == _native.ENKF_SINGULAR_UPDATE and st.level == 3
+
+
+def test_levels_match_model():
+    import reduced_model as M
+    for _, r, v, d, *_ in list(ism_cases())[:6]:
+        g = M.gram_solve(v, d, r)
+        code, st, a, den = _levels_on(g, v.shape[1])
+        a_m, den_m = M.levels(g)
+        assert code == 0
+        assert rel_err(a, a_m) <= 1e-12 and rel_err(den, den_m) <= 1e-13
+
+
+# ---------------------------------------------------------------- analysis_step
+def test_kalman_gain_instances_match_reference():
+    for x, idx, r, perturbed, xa_ref in kalman_cases():
+        h = P.SelectionOperator.from_indices(idx)
+        obs = P.ObservationBatch(y=perturbed[:, 0], perturbed=perturbed, perturbations=perturbed * 0)
+        xa = P.analysis_step(x, obs, h, r, "sherman")
+        assert np.abs(xa - xa_ref).max() <= 1e-12 * max(1.0, np.abs(xa_ref).max())
+        s = oracle.member_deviations(x)
+        hm = np.zeros((idx.size, x.shape[0]))
+        hm[np.arange(idx.size), idx] = 1.0
+        p = s @ s.T
+        gain = p @ hm.T @ np.linalg.inv(hm @ p @ hm.T + np.diag(r))
+        assert np.abs(xa - (x + gain @ (perturbed - hm @ x))).max() <= 1e-9
+
+
+def test_zero_spread_is_identity():
+    x = np.tile(np.arange(6.0)[:, None], (1, 4))
+    h = P.SelectionOperator.from_indices([1, 4])
+    obs = P.ObservationBatch(y=np.array([5.0, -2.0]), perturbed=np.array([[5.0] * 4, [-2.0] * 4]),
+                             perturbations=np.zeros((2, 4)))
+    xa = P.analysis_step(x, obs, h, np.ones(2), "sherman")
+    assert np.array_equal(xa, x)
+
+
+def test_uninformative_observations():
+    g = np.random.Generator(np.random.Philox(1))
+    x = g.standard_normal((10, 4))
+    idx = np.sort(g.choice(10, size=6, replace=False))
+    y = g.standard_normal(6)
+    obs = P.ObservationBatch(y=y, perturbed=y[:, None] + 0.2 * g.standard_normal((6, 4)), perturbations=None)
+    xa = P.analysis_step(x, obs, P.SelectionOperator.from_indices(idx), np.full(6, 1e12), "sherman")
+    assert np.abs(xa - x).max() <= 1e-6 * np.abs(x).max()
+
+
+def test_returns_new_array_inputs_untouched():
+    p = W.config1()
+    x0, y0 = p.x.copy(), p.perturbed.copy()
+    xa = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    assert not np.shares_memory(xa, p.x) and xa.flags.c_contiguous and xa.dtype == np.float64
+    assert np.array_equal(p.x, x0) and np.array_equal(p.perturbed, y0)
+
+
+def test_config1_golden():
+    g = load("configs")
+    h = P.SelectionOperator.from_indices(g["c1_idx"])
+    obs = P.ObservationBatch(y=None, perturbed=g["c1_perturbed"], perturbations=None)
+    xa = P.analysis_step(g["c1_x"], obs, h, g["c1_r"])
+    assert rel_err(xa, g["c1_xa"]) <= XA_TOL
+
+
+@pytest.mark.parametrize("tag", ["c2", "c3", "c4s8"])
+def test_config_goldens(tag):
+    g = load("configs")
+    p = {"c2": lambda: W.Config2Cycler().cycle(), "c3": W.config3, "c4s8": lambda: W.config4(8)}[tag]()
+    xa = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    stride = int(g[f"{tag}_stride"])
+    assert rel_err(xa[::stride], g[f"{tag}_xa_rows"]) <= XA_TOL
+    assert np.abs(xa.sum(axis=0) - g[f"{tag}_xa_colsum"]).max() <= 1e-9 * xa.shape[0] * float(g[f"{tag}_xa_absmax"])
+
+
+@pytest.mark.parametrize("maker", ["config1", "config3", "config4s6", "config4s4", "config5s6"])
+def test_analysis_vs_oracle(maker):
+    p = {"config1": W.config1, "config3": W.config3, "config4s6": lambda: W.config4(6),
+         "config4s4": lambda: W.config4(4), "config5s6": lambda: W.config5(6)}[maker]()
+    xa = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    ref = oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
+    err = rel_err(xa, ref)
+    print(f"{maker}: X^A rel err vs oracle {err:.3e}")
+    assert err <= XA_TOL
+
+
+def test_config2_cycles_open_loop():
+    """Config 2: identical X^B to GPU and oracle at every cycle (open loop),
+    then the GPU analysis drives the next forecast."""
+    cyc = W.Config2Cycler()
+    xa = None
+    for c in range(3):
+        p = cyc.cycle(xa)
+        xa = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+        assert rel_err(xa, oracle.analysis_step(p.x, p.perturbed, None, p.r)) <= XA_TOL
+
+
+def test_device_resident_path_matches_host_path():
+    import torch
+    p = W.config4(8)
+    dev = torch.device("cuda", 0)
+    xa_h = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    x = torch.from_numpy(p.x).to(dev)
+    obs = P.ObservationBatch(y=None, perturbed=torch.from_numpy(p.perturbed).to(dev), perturbations=None)
+    xa_d = P.analysis_step(x, obs, h_of(p), torch.from_numpy(p.r).to(dev))
+    assert xa_d.is_cuda and xa_d.dtype == torch.float64
+    assert np.array_equal(xa_d.cpu().numpy(), xa_h)
+
+
+def test_run_to_run_bitwise_determinism():
+    p = W.config4(6)
+    a = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    b = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    assert np.array_equal(a, b)
+
+
+def test_member_deviations_and_innovations():
+    p = W.config3()
+    s = P.member_deviations(p.x)
+    assert rel_err(s, oracle.member_deviations(p.x)) <= 1e-14
+    d = P.innovations(obs_of(p), h_of(p), p.x)
+    assert np.array_equal(d, oracle.innovations(p.perturbed, p.indices, p.x))
+
+
+def test_device_index_errors_flagged():
+    """Device idx out of range / unsorted is flagged by the Gram kernel (the C
+    ABI's own guard; the Python layer validates before launch)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n = 4
+    plan = _native.Plan(8, 3, n, 0)
+    x = torch.randn((8, n), dtype=torch.float64, device=dev)
+    y = torch.randn((3, n), dtype=torch.float64, device=dev)
+    r = torch.ones(3, dtype=torch.float64, device=dev)
+    out = torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    for bad, code in (([1, 5, 9], _native.ENKF_INDEX_RANGE), ([1, 5, 5], _native.ENKF_INVALID_ARGUMENT)):
+        idx = torch.tensor(bad, dtype=torch.int64, device=dev)
+        st = _native.EnkfStatus()
+        rc = _native.lib().enkf_analysis_f64(plan.handle, x.data_ptr(), y.data_ptr(), idx.data_ptr(),
+                                            r.data_ptr(), out.data_ptr(), s, ctypes.byref(st))
+        assert rc == code, st.message
