@@ -4,8 +4,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <new>
+#include <thread>
+#include <vector>
 
 #include "../../include/enkf_b200.h"
 #include "enkf_kernels.cuh"
@@ -19,6 +22,9 @@ struct enkf_plan {
   int num_sms = 0;
   int splits = 1;
   int64_t rows_per_split = 0;
+  bool use_ws = true;          // warp-specialised TMA kernels (even N, aligned rows)
+  int ws_blocks = 1, ws_ctas_per_block = 1;
+  int64_t ws_rows_per_cta = 0;
   double* partial = nullptr;  // [splits][n][2n]
   double* gram = nullptr;     // [n][2n]
   double* A = nullptr;        // [n][n]
@@ -32,6 +38,12 @@ struct enkf_plan {
   double* hr = nullptr;
   int64_t* hidx = nullptr;
   cudaStream_t hstream = nullptr;
+  // pinned staging ring for pageable host buffers
+  char* ring[2] = {nullptr, nullptr};
+  cudaEvent_t ring_ev[2] = {nullptr, nullptr};
+  bool ring_busy[2] = {false, false};  // an async DMA may still touch the slot
+  int ring_next = 0;
+  size_t ring_bytes = 0;
 };
 
 namespace {
@@ -77,10 +89,40 @@ cudaError_t launch_gram_t(const enkf_plan* p, const double* X, const double* Y,
   return cudaGetLastError();
 }
 
+template <bool ANALYSIS>
+cudaError_t launch_gram_ws_t(const enkf_plan* p, const double* X, const double* Y,
+                             const int64_t* idx, const double* r, cudaStream_t s) {
+  const int n = p->n;
+  const int ld = padded_ld(W_TILE);  // operand tiles are 128 wide whatever n is
+  const size_t smem = gram_ws_smem_bytes(ld);
+  auto kern = gram_ws_kernel<ANALYSIS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kern<<<p->ws_blocks * p->ws_ctas_per_block, W_THREADS, smem, s>>>(
+      X, Y, idx, r, p->n_state, p->n_obs, n, ld, p->ws_ctas_per_block, p->ws_rows_per_cta, p->partial,
+      p->dstatus);
+  return cudaGetLastError();
+}
+
+bool use_ws(const enkf_plan* p, const void* a, const void* b) {
+  return p->use_ws && (p->n % 2 == 0) && aligned16(a) && aligned16(b);
+}
+
 cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, const double* Y,
                         const int64_t* idx, const double* r, double* gram, cudaStream_t s) {
   const int n = p->n;
   if (p->n_obs == 0) return cudaMemsetAsync(gram, 0, sizeof(double) * n * 2 * n, s);
+  if (use_ws(p, X, Y)) {
+    cudaError_t e = analysis ? launch_gram_ws_t<true>(p, X, Y, idx, r, s)
+                             : launch_gram_ws_t<false>(p, X, Y, idx, r, s);
+    if (e != cudaSuccess) return e;
+    const double svv = analysis ? 1.0 / (double)(n - 1) : 1.0;
+    const double svd = analysis ? 1.0 / std::sqrt((double)(n - 1)) : 1.0;
+    const int64_t count = (int64_t)n * 2 * n;
+    gram_ws_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
+                                                                  svv, svd, gram);
+    return cudaGetLastError();
+  }
   const bool vec = (n % 2 == 0) && aligned16(X) && aligned16(Y);
   cudaError_t e;
   if (analysis) e = vec ? launch_gram_t<true, true>(p, X, Y, idx, r, s) : launch_gram_t<true, false>(p, X, Y, idx, r, s);
@@ -106,9 +148,25 @@ template <int NP, int MODE, bool VEC16>
 cudaError_t launch_rowgemm_t(const enkf_plan* p, const double* P, const double* Q, const double* C,
                              const double* r, double* out, int64_t n_rows, cudaStream_t s) {
   const int n = p->n;
-  const int ld = padded_ld(n);
+  const int ld = padded_ld(NP);  // the k loop reads NP >= n columns
   const size_t smem = (size_t)R_STAGES * R_ROWS * ld * sizeof(double);
   auto kern = rowgemm_kernel<NP, MODE, VEC16>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (n_rows + R_ROWS - 1) / R_ROWS;
+  int grid = (int)(ntiles < p->num_sms ? ntiles : p->num_sms);
+  if (grid < 1) return cudaSuccess;
+  kern<<<grid, R_THREADS, smem, s>>>(P, Q, C, r, out, n_rows, n, ld);
+  return cudaGetLastError();
+}
+
+template <int NP, int MODE>
+cudaError_t launch_rowgemm_ws_t(const enkf_plan* p, const double* P, const double* Q, const double* C,
+                                const double* r, double* out, int64_t n_rows, cudaStream_t s) {
+  const int n = p->n;
+  const int ld = padded_ld(NP);  // the k loop reads NP >= n columns
+  const size_t smem = (size_t)R_STAGES * R_ROWS * ld * sizeof(double) + 2 * R_STAGES * sizeof(uint64_t);
+  auto kern = rowgemm_ws_kernel<NP, MODE>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (n_rows + R_ROWS - 1) / R_ROWS;
@@ -122,6 +180,12 @@ template <int MODE>
 cudaError_t launch_rowgemm(const enkf_plan* p, const double* P, const double* Q, const double* C,
                            const double* r, double* out, int64_t n_rows, cudaStream_t s) {
   const int n = p->n;
+  if (use_ws(p, P, out) && (C == nullptr || aligned16(C))) {
+#define ENKF_RW(NPV) \
+    if (n <= NPV) return launch_rowgemm_ws_t<NPV, MODE>(p, P, Q, C, r, out, n_rows, s);
+    ENKF_RW(8) ENKF_RW(16) ENKF_RW(32) ENKF_RW(48) ENKF_RW(64) ENKF_RW(96) ENKF_RW(128)
+#undef ENKF_RW
+  }
   const bool vec = (n % 2 == 0) && aligned16(P) && aligned16(out) && (C == nullptr || aligned16(C));
 #define ENKF_RG(NPV)                                                                   \
   if (n <= NPV) return vec ? launch_rowgemm_t<NPV, MODE, true>(p, P, Q, C, r, out, n_rows, s) \
@@ -129,6 +193,120 @@ cudaError_t launch_rowgemm(const enkf_plan* p, const double* P, const double* Q,
   ENKF_RG(8) ENKF_RG(16) ENKF_RG(32) ENKF_RG(48) ENKF_RG(64) ENKF_RG(96) ENKF_RG(128)
 #undef ENKF_RG
   return cudaErrorInvalidValue;
+}
+
+// ---- host <-> device copies for the host-buffer entry point -----------------
+// Pinned (page-locked or registered) host buffers are DMA'd directly.  Pageable
+// buffers go through a 2 x 256 MiB pinned ring: the host side is copied by a
+// pool of threads (first-touch page faults of fresh numpy arrays are the real
+// cost of pageable transfers and parallelise), the DMA of one ring slot
+// overlaps the host copy of the other.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t min_chunk = (size_t)8 << 20;
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 16) nt = 16;
+  size_t want = (bytes + min_chunk - 1) / min_chunk;
+  if (want < nt) nt = (unsigned)(want ? want : 1);
+  if (nt <= 1) {
+    memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t lo = t * per;
+    if (lo >= bytes) break;
+    const size_t len = (lo + per > bytes) ? bytes - lo : per;
+    th.emplace_back([=] { memcpy((char*)dst + lo, (const char*)src + lo, len); });
+  }
+  for (auto& t : th) t.join();
+}
+
+cudaError_t ensure_ring(enkf_plan* p) {
+  if (p->ring[0]) return cudaSuccess;
+  p->ring_bytes = (size_t)256 << 20;
+  for (int i = 0; i < 2; ++i) {
+    cudaError_t e = cudaMallocHost(&p->ring[i], p->ring_bytes);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ring_ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// Take the next ring slot, waiting until its previous DMA (of any direction,
+// from this or an earlier call) has completed.
+cudaError_t take_slot(enkf_plan* p, int* slot) {
+  *slot = p->ring_next;
+  p->ring_next ^= 1;
+  if (p->ring_busy[*slot]) {
+    cudaError_t e = cudaEventSynchronize(p->ring_ev[*slot]);
+    if (e != cudaSuccess) return e;
+    p->ring_busy[*slot] = false;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t copy_h2d(enkf_plan* p, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if (is_pinned(src)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s);
+  cudaError_t e = ensure_ring(p);
+  if (e != cudaSuccess) return e;
+  for (size_t off = 0; off < bytes;) {
+    const size_t len = bytes - off < p->ring_bytes ? bytes - off : p->ring_bytes;
+    int slot;
+    if ((e = take_slot(p, &slot)) != cudaSuccess) return e;
+    parallel_memcpy(p->ring[slot], (const char*)src + off, len);
+    if ((e = cudaMemcpyAsync((char*)dst + off, p->ring[slot], len, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(p->ring_ev[slot], s)) != cudaSuccess) return e;
+    p->ring_busy[slot] = true;
+    off += len;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t copy_d2h(enkf_plan* p, void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return cudaSuccess;
+  if (is_pinned(dst)) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+  cudaError_t e = ensure_ring(p);
+  if (e != cudaSuccess) return e;
+  const size_t nchunks = (bytes + p->ring_bytes - 1) / p->ring_bytes;
+  int slot_of[2] = {0, 0};
+  auto launch = [&](size_t k) -> cudaError_t {
+    const size_t off = k * p->ring_bytes;
+    const size_t len = bytes - off < p->ring_bytes ? bytes - off : p->ring_bytes;
+    int slot;
+    cudaError_t err = take_slot(p, &slot);
+    if (err != cudaSuccess) return err;
+    slot_of[k & 1] = slot;
+    if ((err = cudaMemcpyAsync(p->ring[slot], (const char*)src + off, len, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return err;
+    if ((err = cudaEventRecord(p->ring_ev[slot], s)) != cudaSuccess) return err;
+    p->ring_busy[slot] = true;
+    return cudaSuccess;
+  };
+  // keep up to two chunks in flight; drain in order
+  for (size_t k = 0; k < nchunks && k < 2; ++k)
+    if ((e = launch(k)) != cudaSuccess) return e;
+  for (size_t k = 0; k < nchunks; ++k) {
+    const int slot = slot_of[k & 1];
+    const size_t off = k * p->ring_bytes;
+    const size_t len = bytes - off < p->ring_bytes ? bytes - off : p->ring_bytes;
+    if ((e = cudaEventSynchronize(p->ring_ev[slot])) != cudaSuccess) return e;
+    p->ring_busy[slot] = false;
+    parallel_memcpy((char*)dst + off, p->ring[slot], len);
+    if (k + 2 < nchunks && (e = launch(k + 2)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 int translate_status(const enkf_plan* p, enkf_status* st) {
@@ -232,8 +410,26 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   p->splits = splits;
   p->rows_per_split = rps;
 
+  // warp-specialised Gram: 128 x 128 blocks, one CTA per SM
+  p->ws_blocks = (2 * n + W_TILE - 1) / W_TILE;
+  int cpb = p->num_sms / p->ws_blocks;
+  if (cpb < 1) cpb = 1;
+  const int64_t max_cpb = (n_obs + W_RT - 1) / W_RT;
+  if (cpb > max_cpb) cpb = (int)(max_cpb > 0 ? max_cpb : 1);
+  int64_t rpc = (n_obs + cpb - 1) / cpb;
+  rpc = (rpc + W_RT - 1) / W_RT * W_RT;
+  if (rpc < W_RT) rpc = W_RT;
+  cpb = (int)((n_obs + rpc - 1) / rpc);
+  if (cpb < 1) cpb = 1;
+  p->ws_ctas_per_block = cpb;
+  p->ws_rows_per_cta = rpc;
+  if (const char* env = getenv("ENKF_DISABLE_WS")) p->use_ws = (env[0] == '0');
+
   const size_t nn = (size_t)n * n;
-  e = cudaMalloc(&p->partial, sizeof(double) * (size_t)splits * 2 * nn);
+  size_t partial_elems = (size_t)splits * 2 * nn;
+  const size_t ws_elems = (size_t)p->ws_blocks * cpb * W_TILE * W_TILE;
+  if (ws_elems > partial_elems) partial_elems = ws_elems;
+  e = cudaMalloc(&p->partial, sizeof(double) * partial_elems);
   if (e == cudaSuccess) e = cudaMalloc(&p->gram, sizeof(double) * 2 * nn);
   if (e == cudaSuccess) e = cudaMalloc(&p->A, sizeof(double) * nn);
   if (e == cudaSuccess) e = cudaMalloc(&p->T, sizeof(double) * nn);
@@ -264,6 +460,10 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->hr);
   cudaFree(p->hidx);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  for (int i = 0; i < 2; ++i) {
+    if (p->ring[i]) cudaFreeHost(p->ring[i]);
+    if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
+  }
   delete p;
 }
 
@@ -351,12 +551,12 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     CUDA_TRY(cudaMalloc(&p->hidx, sizeof(int64_t) * (size_t)p->n_obs + 16), st);
   }
   cudaStream_t s = p->hstream;
-  CUDA_TRY(cudaMemcpyAsync(p->hx, X_h, sizeof(double) * (size_t)p->n_state * n, cudaMemcpyHostToDevice, s), st);
-  CUDA_TRY(cudaMemcpyAsync(p->hy, Y_h, sizeof(double) * (size_t)p->n_obs * n, cudaMemcpyHostToDevice, s), st);
-  CUDA_TRY(cudaMemcpyAsync(p->hr, r_h, sizeof(double) * (size_t)p->n_obs, cudaMemcpyHostToDevice, s), st);
+  CUDA_TRY(copy_h2d(p, p->hx, X_h, sizeof(double) * (size_t)p->n_state * n, s), st);
+  CUDA_TRY(copy_h2d(p, p->hy, Y_h, sizeof(double) * (size_t)p->n_obs * n, s), st);
+  CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
   const int64_t* didx = nullptr;
   if (idx_h) {
-    CUDA_TRY(cudaMemcpyAsync(p->hidx, idx_h, sizeof(int64_t) * (size_t)p->n_obs, cudaMemcpyHostToDevice, s), st);
+    CUDA_TRY(copy_h2d(p, p->hidx, idx_h, sizeof(int64_t) * (size_t)p->n_obs, s), st);
     didx = p->hidx;
   }
   // In place: XA overwrites the device copy of X.
@@ -366,8 +566,13 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     set_status(st, rc, "launch failed");
     return rc;
   }
-  CUDA_TRY(cudaMemcpyAsync(XA_h, p->hx, sizeof(double) * (size_t)p->n_state * n, cudaMemcpyDeviceToHost, s), st);
-  return enkf_plan_sync_status(p, s, st);
+  // Read the status before the (long) copy-out so a failed step raises
+  // without paying for it.
+  int rc2 = enkf_plan_sync_status(p, s, st);
+  if (rc2 != ENKF_OK) return rc2;
+  CUDA_TRY(copy_d2h(p, XA_h, p->hx, sizeof(double) * (size_t)p->n_state * n, s), st);
+  CUDA_TRY(cudaStreamSynchronize(s), st);
+  return ENKF_OK;
 }
 
 int32_t enkf_ism_solve_f64(enkf_plan* p, const double* r, const double* V, const double* D,

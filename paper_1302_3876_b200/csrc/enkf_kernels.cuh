@@ -78,6 +78,47 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+
+// ---- mbarrier / bulk-copy (TMA engine) helpers ------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Bulk (non-tensor) TMA copy global -> shared, completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // Shared-memory row stride (in doubles) for a row of `n` values: >= n, even,
 // and == 4 (mod 16) so the DMMA fragment pattern (row = lane&3 or lane>>2,
 // col = the other) hits 16 distinct 8-byte banks per half-warp.
@@ -286,6 +327,263 @@ gram_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised Gram pass (even N, 16-byte aligned rows): the production
+// kernel.  One CTA per SM computes a 128 x 128 block (column block `cb` of the
+// 2N Gram columns) over a contiguous range of observation rows:
+//   warp 8  (loader)      : idx/r for RT rows, one bulk TMA copy per gathered
+//                           X row (and Y row), completion on load_full[slot]
+//   warps 9-10 (transform): row mean, 1/r, input checks; in place
+//                           A operand w = (x - mean)/r, B operand [s | d]
+//   warps 0-7 (DMMA)      : 64 x 32 warp tiles, m8n8k4 FP64 DMMA over the
+//                           stage's rows (k = observation row)
+// Stages are recycled through load_full / op_full / op_empty mbarriers.
+constexpr int W_RT = 16;       // observation rows per stage
+constexpr int W_STAGES = 4;
+constexpr int W_MMA_WARPS = 8;
+constexpr int W_XFORM_WARPS = 3;
+constexpr int W_THREADS = 32 * (W_MMA_WARPS + 1 + W_XFORM_WARPS);
+constexpr int W_TILE = 128;    // Gram block edge
+
+__host__ __device__ inline size_t gram_ws_smem_bytes(int ld) {
+  return (size_t)W_STAGES * 3 * W_RT * ld * sizeof(double)   // x, y, B buffers
+         + (size_t)W_STAGES * W_RT * (sizeof(double) + sizeof(int))  // rinv, valid
+         + 3 * W_STAGES * sizeof(uint64_t) + 64;
+}
+
+template <bool ANALYSIS>
+__global__ void __launch_bounds__(W_THREADS, 1)
+gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+               const int64_t* __restrict__ idx, const double* __restrict__ r,
+               int64_t n_state, int64_t n_obs, int n, int ld, int ctas_per_block,
+               int64_t rows_per_cta, double* __restrict__ partial, DevStatus* __restrict__ status) {
+  extern __shared__ __align__(128) unsigned char wsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cb = blockIdx.x / ctas_per_block;       // Gram column block
+  const int part = blockIdx.x % ctas_per_block;     // row range
+  const int nb = (2 * n + W_TILE - 1) / W_TILE;
+  const int col0 = cb * W_TILE;
+  const bool needY = (col0 + W_TILE > n);           // block touches D columns
+  const bool checker = (cb == nb - 1);
+  const int64_t row_begin = (int64_t)part * rows_per_cta;
+  const int64_t row_end = row_begin + rows_per_cta < n_obs ? row_begin + rows_per_cta : n_obs;
+  const int nstages = row_end > row_begin ? (int)((row_end - row_begin + W_RT - 1) / W_RT) : 0;
+
+  const int stage_elems = W_RT * ld;
+  double* xb = reinterpret_cast<double*>(wsm);
+  double* yb = xb + W_STAGES * stage_elems;
+  double* bb = yb + W_STAGES * stage_elems;
+  double* rinv_s = bb + W_STAGES * stage_elems;
+  int* valid_s = reinterpret_cast<int*>(rinv_s + W_STAGES * W_RT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(valid_s + W_STAGES * W_RT) + 15) & ~uintptr_t(15));
+  uint64_t* load_full = bars;
+  uint64_t* op_full = bars + W_STAGES;
+  uint64_t* op_empty = bars + 2 * W_STAGES;
+
+  if (tid == 0) {
+    for (int i = 0; i < W_STAGES; ++i) {
+      mbar_init(&load_full[i], 1);
+      mbar_init(&op_full[i], 32 * W_XFORM_WARPS);
+      mbar_init(&op_empty[i], 32 * W_MMA_WARPS);
+    }
+    fence_mbar_init();
+  }
+  // zero the padding columns of every buffer once (operands beyond n stay 0)
+  for (int e = tid; e < 3 * W_STAGES * W_RT; e += blockDim.x)
+    for (int c = n; c < ld; ++c) xb[(size_t)e * ld + c] = 0.0;
+  __syncthreads();
+
+  if (warp == W_MMA_WARPS) {
+    // ------------------------------------------------------------- loader
+    int flags = 0;
+    for (int t = 0; t < nstages; ++t) {
+      const int slot = t % W_STAGES;
+      if (t >= W_STAGES) mbar_wait(&op_empty[slot], ((t / W_STAGES) - 1) & 1);
+      fence_proxy_async();
+      const int64_t g = row_begin + (int64_t)t * W_RT + lane;
+      bool valid = lane < W_RT && g < row_end;
+      int64_t src = g;
+      double rv = 1.0;
+      if (valid) {
+        rv = r[g];
+        if (ANALYSIS && idx != nullptr) {
+          src = idx[g];
+          if (checker) {
+            const int64_t prev = g > 0 ? idx[g - 1] : -1;
+            if (prev >= src) flags |= FLAG_IDX_ORDER;
+          }
+          if (src < 0 || src >= n_state) { flags |= FLAG_IDX_RANGE; valid = false; }
+        }
+        if (checker) {
+          if (!isfinite(rv)) flags |= FLAG_NONFINITE;
+          else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
+        }
+      }
+      if (lane < W_RT) {
+        rinv_s[slot * W_RT + lane] = valid ? 1.0 / rv : 0.0;
+        valid_s[slot * W_RT + lane] = valid ? 1 : 0;
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      const uint32_t row_bytes = (uint32_t)n * 8u;
+      const uint32_t total = (uint32_t)__popc(vmask) * row_bytes * (needY ? 2u : 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&load_full[slot], total);
+      __syncwarp();
+      if (valid) {
+        bulk_g2s(xb + slot * stage_elems + lane * ld, X + src * (int64_t)n, row_bytes, &load_full[slot]);
+        if (needY) bulk_g2s(yb + slot * stage_elems + lane * ld, Y + g * (int64_t)n, row_bytes, &load_full[slot]);
+      }
+    }
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 8);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 4);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 2);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 1);
+    if (lane == 0 && flags) atomicOr(&status->flags, flags);
+    return;
+  }
+
+  if (warp > W_MMA_WARPS) {
+    // ---------------------------------------------------------- transforms
+    // Each warp handles rows tw, tw + 3, ... two at a time (independent
+    // load -> shuffle-reduce -> scale chains in flight).
+    const int tw = warp - W_MMA_WARPS - 1;
+    const double inv_n = 1.0 / (double)n;
+    int flags = 0;
+    constexpr int CPL = (W_TILE + 31) / 32;  // columns per lane (4 for n <= 128)
+    for (int t = 0; t < nstages; ++t) {
+      const int slot = t % W_STAGES;
+      mbar_wait(&load_full[slot], (t / W_STAGES) & 1);
+      double* xs = xb + slot * stage_elems;
+      double* ys = yb + slot * stage_elems;
+      double* bs = bb + slot * stage_elems;
+      for (int r0 = tw; r0 < W_RT; r0 += 2 * W_XFORM_WARPS) {
+        const int r1 = r0 + W_XFORM_WARPS;
+        const bool has1 = r1 < W_RT;
+        double xv[2][CPL], bx[2][CPL], by[2][CPL], sum[2] = {0.0, 0.0};
+        bool valid[2];
+        double ri[2];
+        bool bad = false;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int rr = u ? r1 : r0;
+          valid[u] = (u == 0 || has1) && valid_s[slot * W_RT + rr] != 0;
+          ri[u] = (u == 0 || has1) ? rinv_s[slot * W_RT + rr] : 0.0;
+          const double* xr = xs + rr * ld;
+          const double* yr = ys + rr * ld;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int c = lane + 32 * q;
+            xv[u][q] = (valid[u] && c < n) ? xr[c] : 0.0;
+            sum[u] += xv[u][q];
+            if (checker && valid[u] && c < n) bad |= !isfinite(xv[u][q]) || !isfinite(yr[c]);
+            const int gc = col0 + c;
+            bx[u][q] = 0.0;
+            by[u][q] = 0.0;
+            if (valid[u]) {
+              if (gc < n) bx[u][q] = xr[gc];
+              else if (gc < 2 * n) { bx[u][q] = xr[gc - n]; by[u][q] = yr[gc - n]; }
+            }
+          }
+        }
+        if (checker && __any_sync(0xffffffffu, bad)) flags |= FLAG_NONFINITE;
+        double mean[2] = {0.0, 0.0};
+        if (ANALYSIS) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sum[0] += __shfl_xor_sync(0xffffffffu, sum[0], o);
+            sum[1] += __shfl_xor_sync(0xffffffffu, sum[1], o);
+          }
+          mean[0] = sum[0] * inv_n;
+          mean[1] = sum[1] * inv_n;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u == 1 && !has1) break;
+          const int rr = u ? r1 : r0;
+          double* xr = xs + rr * ld;
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            const int c = lane + 32 * q;
+            if (c < n) xr[c] = valid[u] ? (xv[u][q] - mean[u]) * ri[u] : 0.0;  // A operand (w)
+            const int gc = col0 + c;
+            double b = 0.0;
+            if (valid[u]) {
+              if (gc < n) b = ANALYSIS ? bx[u][q] - mean[u] : bx[u][q];
+              else if (gc < 2 * n) b = ANALYSIS ? by[u][q] - bx[u][q] : by[u][q];
+            }
+            bs[rr * ld + c] = b;
+          }
+        }
+      }
+      fence_proxy_async();  // generic writes of this slot precede its next TMA refill
+      mbar_arrive(&op_full[slot]);
+    }
+    if (flags) atomicOr(&status->flags, flags);
+    return;
+  }
+
+  // ------------------------------------------------------------------ DMMA
+  const int wm = warp & 1, wn = warp >> 1;   // 64-row x 32-col warp tiles
+  const bool active = (64 * wm < n) && (col0 + 32 * wn < 2 * n);
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int arow = lane & 3, acol = 64 * wm + (lane >> 2), bcol = 32 * wn + (lane >> 2);
+  for (int t = 0; t < nstages; ++t) {
+    const int slot = t % W_STAGES;
+    mbar_wait(&op_full[slot], (t / W_STAGES) & 1);
+    if (active) {
+      const double* as = xb + slot * stage_elems;
+      const double* bsm = bb + slot * stage_elems;
+#pragma unroll
+      for (int ks = 0; ks < W_RT / 4; ++ks) {
+        const int row = 4 * ks + arow;
+        double a[8], b[4];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) a[mt] = as[row * ld + acol + 8 * mt];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = bsm[row * ld + bcol + 8 * nt];
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+      }
+    }
+    mbar_arrive(&op_empty[slot]);
+  }
+  // partial tile [blockIdx.x][128][128]
+  double* out = partial + (size_t)blockIdx.x * W_TILE * W_TILE;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const int i = 64 * wm + 8 * mt + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = 32 * wn + 8 * nt + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + i * W_TILE + j) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    }
+  }
+}
+
+// Fixed-order reduction of the warp-specialised partial tiles into the Gram.
+__global__ void gram_ws_reduce(const double* __restrict__ partial, int n, int ctas_per_block,
+                               double s_vv, double s_vd, double* __restrict__ gram) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t count = (int64_t)n * 2 * n;
+  if (e >= count) return;
+  const int i = (int)(e / (2 * n)), c = (int)(e % (2 * n));
+  const int cb = c / W_TILE, j = c % W_TILE;
+  const double* src = partial + (size_t)cb * ctas_per_block * W_TILE * W_TILE + i * W_TILE + j;
+  double s = 0.0;
+  for (int k = 0; k < ctas_per_block; ++k) s += src[(size_t)k * W_TILE * W_TILE];
+  gram[e] = s * (c < n ? s_vv : s_vd);
+}
+
 // Fixed-order reduction of the split partials; scale V'R^-1V by s_vv and
 // V'R^-1D by s_vd (1/(N-1) and 1/sqrt(N-1) in analysis mode).
 __global__ void gram_reduce(const double* __restrict__ partial, int splits, int n,
@@ -300,17 +598,24 @@ __global__ void gram_reduce(const double* __restrict__ partial, int splits, int 
 }
 
 // ---------------------------------------------------------------------------
-// The N Sherman-Morrison levels on the Gram (one CTA, shared memory).
+// The N Sherman-Morrison levels on the Gram (one CTA of 1024 threads).
 // Gamma_k[i][c] = v_i' W_k^-1 g_c with W_k = R + sum_{j<=k} v_j v_j':
 //   den_k = 1 + Gamma_{k-1}[k][k]                       (sherman.py:172)
 //   |den_k| < 1e-14  ->  SingularUpdateError(k+1, den_k) (sherman.py:173-174)
 //   Gamma_k[i][c] = Gamma_{k-1}[i][c] - Gamma_{k-1}[i][k] Gamma_{k-1}[k][c] / den_k
 // for every later column c (the rank-one update col -= h_k (v_k'col) of
 // sherman.py:182-187/208-214 seen through v_i').  The V'V block is symmetric at
-// every level and is kept packed (upper triangle); after N levels the V'D block
-// is A = V'Z.
+// every level: it is kept packed (upper triangle) in shared memory, and its
+// column k doubles as the pivot row (pc).  The V'D block (A = V'Z after the
+// last level) lives in registers: warp w owns rows 4w..4w+3, lane l owns
+// columns 4l..4l+3.  Pivot data for level k+1 is written by the threads that
+// produce it during level k (double-buffered), so each level costs one barrier.
+__host__ __device__ inline int64_t levels_vv_doubles(int n) {
+  const int64_t packed = (int64_t)n * (n + 1) / 2;
+  return packed > 32 * (int64_t)n ? packed : 32 * (int64_t)n;  // also holds the column partials
+}
 __host__ __device__ inline int64_t levels_smem_doubles(int n) {
-  return (int64_t)n * (n + 1) / 2 + (int64_t)n * n + 3 * (int64_t)n + 8;
+  return levels_vv_doubles(n) + 4 * (int64_t)n + 8;
 }
 
 __global__ void __launch_bounds__(1024, 1)
@@ -319,70 +624,119 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
                   double* __restrict__ den_out, DevStatus* __restrict__ status) {
   extern __shared__ __align__(16) double lsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
   double* vv = lsm;                               // packed: p(i,c) = c(c+1)/2 + i, i <= c
-  double* vd = vv + (int64_t)n * (n + 1) / 2;     // [n][n]
-  double* pc = vd + (int64_t)n * n;               // pivot column Gamma[.][k]
-  double* q = pc + n;                             // scaled pivot row: [0,n) V part, [n,2n) D part
+  double* pcb = vv + levels_vv_doubles(n);        // [2][n] pivot column Gamma[.][k]
+  double* qdb = pcb + 2 * n;                      // [2][n] pivot row of V'D: Gamma[k][n + c]
   auto P = [](int i, int c) { return c * (c + 1) / 2 + i; };
-
   const int n2 = 2 * n;
-  for (int e = tid; e < n * n2; e += blockDim.x) {
-    const int i = e / n2, c = e - i * n2;
-    const double g = gram[e];
-    if (c < n) {
-      if (i <= c) vv[P(i, c)] = g;
-    } else {
-      vd[i * n + (c - n)] = g;
+
+  // V'D block in registers.
+  double vd[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = 4 * warp + a, c = 4 * lane + b;
+      vd[a][b] = (i < n && c < n) ? gram[(int64_t)i * n2 + n + c] : 0.0;
     }
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, c = e - i * n;
+    if (i <= c) vv[P(i, c)] = gram[(int64_t)i * n2 + c];
+  }
+  // level-0 pivot data: pc[i] = Gamma[i][0] = Gamma[0][i]; qd = V'D row 0
+  for (int i = tid; i < n; i += blockDim.x) {
+    pcb[i] = gram[i];
+    qdb[i] = gram[n + i];
   }
   __syncthreads();
 
   for (int k = 0; k < n; ++k) {
-    const double dk = 1.0 + vv[P(k, k)];
+    const int cur = k & 1, nxt = cur ^ 1;
+    const double* pc = pcb + cur * n;
+    const double* qd = qdb + cur * n;
+    double* pcn = pcb + nxt * n;
+    double* qdn = qdb + nxt * n;
+    const double dk = 1.0 + pc[k];
     if (fabs(dk) < kSingularTol) {
-      if (tid == 0) {
-        if (!(atomicOr(&status->flags, FLAG_SINGULAR) & FLAG_SINGULAR)) {
-          status->level = k + 1;
-          status->den = dk;
-        }
+      if (tid == 0 && !(atomicOr(&status->flags, FLAG_SINGULAR) & FLAG_SINGULAR)) {
+        status->level = k + 1;
+        status->den = dk;
       }
-      return;
+      return;  // uniform: every thread read the same dk
     }
     if (tid == 0 && den_out) den_out[k] = dk;
     const double inv = 1.0 / dk;
-    for (int i = tid; i < n; i += blockDim.x) pc[i] = (i <= k) ? vv[P(i, k)] : vv[P(k, i)];
-    for (int c = tid; c < n2; c += blockDim.x) {
-      if (c < n) q[c] = (c > k) ? vv[P(k, c)] * inv : 0.0;
-      else q[c] = vd[k * n + (c - n)] * inv;
-    }
-    __syncthreads();
-    for (int c = k + 1 + warp; c < n; c += nwarps) {
-      const double qc = q[c];
+    // V'V: columns c > k, rows i <= c.
+#pragma unroll 1
+    for (int c = k + 1 + warp; c < n; c += 32) {
+      const double qc = pc[c] * inv;
       double* col = vv + P(0, c);
-      for (int i = lane; i <= c; i += 32) col[i] -= pc[i] * qc;
+#pragma unroll 1
+      for (int i = lane; i <= c; i += 32) {
+        const double val = col[i] - pc[i] * qc;
+        col[i] = val;
+        if (c == k + 1) pcn[i] = val;             // column k+1, rows <= k+1
+        else if (i == k + 1) pcn[c] = val;        // row k+1 = column k+1 by symmetry
+      }
     }
-    for (int i = warp; i < n; i += nwarps) {
-      const double pi = pc[i];
-      double* row = vd + i * n;
-      for (int c = lane; c < n; c += 32) row[c] -= pi * q[n + c];
+    // V'D: all rows, all columns (registers).
+    double qs[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = 4 * lane + b;
+      qs[b] = c < n ? qd[c] * inv : 0.0;
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int i = 4 * warp + a;
+      const double pr = i < n ? pc[i] : 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) vd[a][b] -= pr * qs[b];
+    }
+    if ((k + 1) >> 2 == warp) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (4 * warp + a == k + 1) {
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            if (4 * lane + b < n) qdn[4 * lane + b] = vd[a][b];
+        }
     }
     __syncthreads();
   }
 
   // A = V'Z; T = I + cscale (A - 1 colmean(A)').
-  for (int e = tid; e < n * n; e += blockDim.x) A[e] = vd[e];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = 4 * warp + a, c = 4 * lane + b;
+      if (i < n && c < n) A[i * n + c] = vd[a][b];
+    }
   if (T != nullptr) {
-    for (int c = tid; c < n; c += blockDim.x) {
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s += vd[i * n + c];
-      pc[c] = s / (double)n;
+    // column means in a fixed order: per-warp partial over its 4 rows, then
+    // a serial sum over warps
+    double* cpart = vv;  // the packed V'V block is dead now; it holds >= 32 n doubles
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int c = 4 * lane + b;
+      if (c < n) cpart[warp * n + c] = vd[0][b] + vd[1][b] + vd[2][b] + vd[3][b];
     }
     __syncthreads();
-    for (int e = tid; e < n * n; e += blockDim.x) {
-      const int i = e / n, c = e - i * n;
-      T[e] = (i == c ? 1.0 : 0.0) + cscale * (vd[e] - pc[c]);
+    double* cm = pcb;
+    for (int c = tid; c < n; c += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < 32; ++w) s += cpart[w * n + c];
+      cm[c] = s / (double)n;
     }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = 4 * warp + a, c = 4 * lane + b;
+        if (i < n && c < n) T[i * n + c] = (i == c ? 1.0 : 0.0) + cscale * (vd[a][b] - cm[c]);
+      }
   }
 }
 
@@ -494,6 +848,116 @@ rowgemm_kernel(const double* __restrict__ P, const double* __restrict__ Q,
     }
   }
   cp_async_wait<0>();
+}
+
+
+// TMA-fed row GEMM (even N, 16-byte aligned rows): the production anomaly-
+// update / Z-pass kernel.  Thread 0 streams 32-row tiles of P into a 4-slot
+// ring with one bulk TMA copy per row (mbarrier full/empty pairs), refilling a
+// slot as soon as all 8 warps have released it; the warps keep the N x N
+// operand Q stationary in registers (no producer warp, so each thread keeps
+// the full 255-register budget) and run the m8n8k4 FP64 DMMA, releasing each
+// slot before their epilogue stores.
+template <int NP, int MODE>
+__global__ void __launch_bounds__(R_THREADS, 1)
+rowgemm_ws_kernel(const double* __restrict__ P, const double* __restrict__ Q,
+                  const double* __restrict__ C, const double* __restrict__ r,
+                  double* __restrict__ out, int64_t n_rows, int n, int ld) {
+  constexpr int KT = NP / 4;
+  constexpr int NTT = NP / 8;
+  constexpr int NTW = (NTT + 7) / 8;
+  extern __shared__ __align__(128) unsigned char rwsm[];
+  double* ring = reinterpret_cast<double*>(rwsm);
+  const int stage_elems = R_ROWS * ld;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + R_STAGES * stage_elems);
+  uint64_t* empty = full + R_STAGES;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntiles = (n_rows + R_ROWS - 1) / R_ROWS;
+  const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (tid == 0) {
+    for (int i = 0; i < R_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], R_THREADS);
+    }
+    fence_mbar_init();
+  }
+  for (int e = tid; e < R_STAGES * R_ROWS; e += blockDim.x)
+    for (int c = n; c < ld; ++c) ring[(size_t)e * ld + c] = 0.0;
+  __syncthreads();
+
+  // issue the bulk copies of local tile `it` (thread 0 only)
+  auto issue = [&](int64_t it) {
+    const int slot = (int)(it % R_STAGES);
+    if (it >= R_STAGES) mbar_wait(&empty[slot], (uint32_t)(((it / R_STAGES) - 1) & 1));
+    fence_proxy_async();
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    const int64_t g0 = tile * R_ROWS;
+    const int rows = (int)(n_rows - g0 < R_ROWS ? n_rows - g0 : R_ROWS);
+    const uint32_t row_bytes = (uint32_t)n * 8u;
+    mbar_arrive_expect_tx(&full[slot], (uint32_t)rows * row_bytes);
+    for (int rr = 0; rr < rows; ++rr)
+      bulk_g2s(ring + slot * stage_elems + rr * ld, P + (g0 + rr) * (int64_t)n, row_bytes, &full[slot]);
+  };
+  if (tid == 0)
+    for (int64_t it = 0; it < R_STAGES - 1 && it < my_tiles; ++it) issue(it);
+
+  double b[KT][NTW];
+#pragma unroll
+  for (int ks = 0; ks < KT; ++ks)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      const int k = 4 * ks + (lane & 3);
+      const int col = 8 * (warp + 8 * j) + (lane >> 2);
+      b[ks][j] = (k < n && col < n && warp + 8 * j < NTT) ? Q[k * n + col] : 0.0;
+    }
+
+  for (int64_t it = 0; it < my_tiles; ++it) {
+    if (tid == 0 && it + R_STAGES - 1 < my_tiles) issue(it + R_STAGES - 1);
+    const int slot = (int)(it % R_STAGES);
+    mbar_wait(&full[slot], (uint32_t)((it / R_STAGES) & 1));
+    const int64_t tile = blockIdx.x + it * gridDim.x;
+    const double* ps = ring + slot * stage_elems;
+    double acc[4][NTW][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) acc[mt][j][0] = acc[mt][j][1] = 0.0;
+    if (warp < NTT) {
+#pragma unroll
+      for (int ks = 0; ks < KT; ++ks) {
+        double a[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) a[mt] = ps[(mt * 8 + (lane >> 2)) * ld + 4 * ks + (lane & 3)];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int j = 0; j < NTW; ++j) dmma884(acc[mt][j][0], acc[mt][j][1], a[mt], b[ks][j]);
+      }
+    }
+    mbar_arrive(&empty[slot]);
+    if (warp < NTT) {
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int64_t g = tile * R_ROWS + mt * 8 + (lane >> 2);
+        if (g >= n_rows) continue;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+          if (warp + 8 * j >= NTT) continue;
+          const int col = 8 * (warp + 8 * j) + 2 * (lane & 3);
+          if (col >= n) continue;
+          double o0 = acc[mt][j][0], o1 = acc[mt][j][1];
+          if (MODE == 1) {
+            const double rv = r[g];
+            const double2 cv = *reinterpret_cast<const double2*>(C + g * n + col);
+            o0 = (cv.x - o0) / rv;
+            o1 = (cv.y - o1) / rv;
+          }
+          *reinterpret_cast<double2*>(out + g * (int64_t)n + col) = make_double2(o0, o1);
+        }
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

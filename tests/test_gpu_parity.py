@@ -275,3 +275,77 @@ def test_device_index_errors_flagged():
         rc = _native.lib().enkf_analysis_f64(plan.handle, x.data_ptr(), y.data_ptr(), idx.data_ptr(),
                                             r.data_ptr(), out.data_ptr(), s, ctypes.byref(st))
         assert rc == code, st.message
+
+
+def _staged_analysis(plan, x, y, idx, r):
+    import torch
+    n = x.shape[1]
+    dev = x.device
+    gram = torch.empty((n, 2 * n), dtype=torch.float64, device=dev)
+    a = torch.empty((n, n), dtype=torch.float64, device=dev)
+    t = torch.empty((n, n), dtype=torch.float64, device=dev)
+    out = torch.empty_like(x)
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    assert lib.enkf_plan_reset_status(plan.handle, s) == 0
+    assert lib.enkf_ism_gram_f64(plan.handle, x.data_ptr(), y.data_ptr(), 0 if idx is None else idx.data_ptr(),
+                                 r.data_ptr(), gram.data_ptr(), s) == 0
+    assert lib.enkf_ism_levels_f64(plan.handle, gram.data_ptr(), a.data_ptr(), t.data_ptr(), None, s) == 0
+    assert lib.enkf_anomaly_update_f64(plan.handle, x.data_ptr(), t.data_ptr(), out.data_ptr(), x.shape[0], s) == 0
+    st = _native.EnkfStatus()
+    _native.raise_for_status(lib.enkf_plan_sync_status(plan.handle, s, ctypes.byref(st)), st)
+    return gram.cpu().numpy(), out.cpu().numpy()
+
+
+@pytest.mark.parametrize("maker", ["config4s8", "config3"])
+def test_tma_kernels_match_generic_kernels(maker, monkeypatch):
+    """The warp-specialised TMA kernels (production) and the generic cp.async
+    kernels (odd N / unaligned fallback) agree."""
+    import torch
+    p = {"config4s8": lambda: W.config4(8), "config3": W.config3}[maker]()
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(p.x).to(dev)
+    y = torch.from_numpy(p.perturbed).to(dev)
+    r = torch.from_numpy(p.r).to(dev)
+    idx = None if p.indices is None else torch.from_numpy(p.indices).to(dev)
+    ns, nobs, n = p.shape
+    plan_ws = _native.Plan(ns, nobs, n, 0)
+    monkeypatch.setenv("ENKF_DISABLE_WS", "1")
+    plan_gen = _native.Plan(ns, nobs, n, 0)
+    g1, xa1 = _staged_analysis(plan_ws, x, y, idx, r)
+    g2, xa2 = _staged_analysis(plan_gen, x, y, idx, r)
+    assert rel_err(g1, g2) <= 1e-13
+    assert rel_err(xa1, xa2) <= 1e-12
+    ref = oracle.analysis_step(p.x, p.perturbed, p.indices, p.r)
+    assert rel_err(xa1, ref) <= XA_TOL and rel_err(xa2, ref) <= XA_TOL
+
+
+@pytest.mark.parametrize("ws", ["0", "1"])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8, 16, 20, 33, 50, 64, 66, 96, 100, 127, 128])
+def test_solve_ensemble_size_sweep(n, ws, monkeypatch):
+    """Every ensemble size up to the maximum, through both kernel families
+    (TMA/warp-specialised for even N, generic cp.async otherwise)."""
+    import torch
+    import reduced_model as M
+    monkeypatch.setenv("ENKF_DISABLE_WS", ws)
+    dev = torch.device("cuda", 0)
+    lib = _native.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    for nobs in (5, 50, 1000):
+        g = np.random.Generator(np.random.Philox(n * 1000 + nobs))
+        r = g.uniform(0.5, 2, nobs)
+        v = g.standard_normal((nobs, n))
+        d = g.standard_normal((nobs, n))
+        plan = _native.Plan(0, nobs, n, 0)
+        z = torch.empty((nobs, n), dtype=torch.float64, device=dev)
+        a = torch.empty((n, n), dtype=torch.float64, device=dev)
+        rt, vt, dt = (torch.from_numpy(t).to(dev) for t in (r, v, d))
+        st = _native.EnkfStatus()
+        rc = lib.enkf_ism_solve_f64(plan.handle, rt.data_ptr(), vt.data_ptr(), dt.data_ptr(), z.data_ptr(),
+                                    a.data_ptr(), s, ctypes.byref(st))
+        assert rc == 0, st.message
+        zm, am = M.solve(r, v, d)
+        assert rel_err(z.cpu().numpy(), zm) <= 1e-11, (n, nobs)
+        assert rel_err(a.cpu().numpy(), am) <= 1e-10, (n, nobs)
+        z_or, _ = oracle.solve_sherman(r, v, d)
+        assert rel_err(z.cpu().numpy(), z_or) <= Z_TOL, (n, nobs)
