@@ -153,13 +153,9 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- GPU leg
 def run_ours(args):
-    import ctypes
-
-    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_1302_3876_b200 import _native
     from paper_1302_3876_b200 import workloads as W
     from paper_1302_3876_b200.build import build
 
@@ -189,41 +185,16 @@ def run_ours(args):
     x, yv, r, idx = shard["x"], shard["perturbed"], shard["r"], shard["idx"]
     ns_loc, nobs_loc = x.shape[0], yv.shape[0]
     xa = torch.empty_like(x)
-    gram = torch.empty((n, 2 * n), dtype=torch.float64, device=dev)
-    a = torch.empty((n, n), dtype=torch.float64, device=dev)
-    t = torch.empty((n, n), dtype=torch.float64, device=dev)
-    den = torch.empty(n, dtype=torch.float64, device=dev)
-    plan = _native.Plan(ns_loc, nobs_loc, n, local)
-    lib = _native.lib()
+    from paper_1302_3876_b200.distributed import CudaStages, ShardedAnalysis
+    runner = ShardedAnalysis(CudaStages(ns_loc, nobs_loc, n, dev))
     stream = torch.cuda.current_stream(dev)
-    sp = stream.cuda_stream
 
     def step(ev=None):
-        lib.enkf_plan_reset_status(plan.handle, sp)
-        if ev:
-            ev[0].record(stream)
-        assert lib.enkf_ism_gram_f64(plan.handle, x.data_ptr(), yv.data_ptr(), idx.data_ptr(),
-                                     r.data_ptr(), gram.data_ptr(), sp) == 0
-        if ev:
-            ev[1].record(stream)
-        if world > 1:
-            dist.all_reduce(gram)
-        if ev:
-            ev[2].record(stream)
-        assert lib.enkf_ism_levels_f64(plan.handle, gram.data_ptr(), a.data_ptr(), t.data_ptr(),
-                                       den.data_ptr(), sp) == 0
-        if ev:
-            ev[3].record(stream)
-        assert lib.enkf_anomaly_update_f64(plan.handle, x.data_ptr(), t.data_ptr(), xa.data_ptr(),
-                                           ns_loc, sp) == 0
-        if ev:
-            ev[4].record(stream)
+        runner.step(x, yv, idx, r, xa, check=False, events=ev)
 
     for _ in range(args.warmup):
         step()
-    st = _native.EnkfStatus()
-    code = lib.enkf_plan_sync_status(plan.handle, sp, ctypes.byref(st))
-    _native.raise_for_status(code, st, "warmup step")
+    runner.raise_for_status()
 
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
     if world > 1:
@@ -239,8 +210,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     ms = start.elapsed_time(stop)
-    code = lib.enkf_plan_sync_status(plan.handle, sp, ctypes.byref(st))
-    _native.raise_for_status(code, st, "timed steps")
+    runner.raise_for_status()
     t_gram = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
     t_ar = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     t_lev = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps

@@ -397,23 +397,35 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 
   if (warp == W_MMA_WARPS) {
     // ------------------------------------------------------------- loader
+    // idx / r of stage t+1 are fetched before waiting for the slot of stage t
     int flags = 0;
-    for (int t = 0; t < nstages; ++t) {
-      const int slot = t % W_STAGES;
-      if (t >= W_STAGES) mbar_wait(&op_empty[slot], ((t / W_STAGES) - 1) & 1);
-      fence_proxy_async();
+    auto fetch = [&](int t, bool& valid, int64_t& src, double& rv, int64_t& prev) {
       const int64_t g = row_begin + (int64_t)t * W_RT + lane;
-      bool valid = lane < W_RT && g < row_end;
-      int64_t src = g;
-      double rv = 1.0;
+      valid = t < nstages && lane < W_RT && g < row_end;
+      src = g;
+      rv = 1.0;
+      prev = -1;
       if (valid) {
         rv = r[g];
         if (ANALYSIS && idx != nullptr) {
           src = idx[g];
-          if (checker) {
-            const int64_t prev = g > 0 ? idx[g - 1] : -1;
-            if (prev >= src) flags |= FLAG_IDX_ORDER;
-          }
+          if (checker && g > 0) prev = idx[g - 1];
+        }
+      }
+    };
+    bool nvalid;
+    int64_t nsrc, nprev;
+    double nrv;
+    fetch(0, nvalid, nsrc, nrv, nprev);
+    for (int t = 0; t < nstages; ++t) {
+      const int slot = t % W_STAGES;
+      bool valid = nvalid;
+      const int64_t src = nsrc, prev = nprev, g = row_begin + (int64_t)t * W_RT + lane;
+      const double rv = nrv;
+      fetch(t + 1, nvalid, nsrc, nrv, nprev);
+      if (valid) {
+        if (ANALYSIS && idx != nullptr) {
+          if (checker && g > 0 && prev >= src) flags |= FLAG_IDX_ORDER;
           if (src < 0 || src >= n_state) { flags |= FLAG_IDX_RANGE; valid = false; }
         }
         if (checker) {
@@ -421,6 +433,8 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
           else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
         }
       }
+      if (t >= W_STAGES) mbar_wait(&op_empty[slot], ((t / W_STAGES) - 1) & 1);
+      fence_proxy_async();
       if (lane < W_RT) {
         rinv_s[slot * W_RT + lane] = valid ? 1.0 / rv : 0.0;
         valid_s[slot * W_RT + lane] = valid ? 1 : 0;
@@ -451,6 +465,10 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     // load -> shuffle-reduce -> scale chains in flight).
     const int tw = warp - W_MMA_WARPS - 1;
     const double inv_n = 1.0 / (double)n;
+    // a block is "pure" when all of its 128 columns are V columns or all are
+    // D columns of one aligned 128-wide slice (n == 128)
+    const bool pure = (n == W_TILE);
+    const bool pure_d = pure && col0 >= n;
     int flags = 0;
     constexpr int CPL = (W_TILE + 31) / 32;  // columns per lane (4 for n <= 128)
     for (int t = 0; t < nstages; ++t) {
@@ -459,6 +477,68 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
       double* xs = xb + slot * stage_elems;
       double* ys = yb + slot * stage_elems;
       double* bs = bb + slot * stage_elems;
+      if (pure) {
+        // Pure block (all V or all D columns, n == 128 in practice): lane owns
+        // columns {2l, 2l+1, 64+2l, 65+2l}; 16-byte shared accesses; input
+        // checks folded into the row sums (a non-finite entry makes them
+        // non-finite).
+        for (int r0 = tw; r0 < W_RT; r0 += 2 * W_XFORM_WARPS) {
+          const int r1 = r0 + W_XFORM_WARPS;
+          const bool has1 = r1 < W_RT;
+          double2 xv[2][2], yv[2][2];
+          double sx[2], sy[2], ri[2];
+          bool valid[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int rr = u ? (has1 ? r1 : r0) : r0;
+            valid[u] = valid_s[slot * W_RT + rr] != 0;
+            ri[u] = rinv_s[slot * W_RT + rr];
+            const double* xr = xs + rr * ld;
+            const double* yr = ys + rr * ld;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              xv[u][h] = *reinterpret_cast<const double2*>(xr + 64 * h + 2 * lane);
+              yv[u][h] = pure_d ? *reinterpret_cast<const double2*>(yr + 64 * h + 2 * lane) : make_double2(0.0, 0.0);
+            }
+            sx[u] = (xv[u][0].x + xv[u][0].y) + (xv[u][1].x + xv[u][1].y);
+            sy[u] = (yv[u][0].x + yv[u][0].y) + (yv[u][1].x + yv[u][1].y);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sx[0] += __shfl_xor_sync(0xffffffffu, sx[0], o);
+            sx[1] += __shfl_xor_sync(0xffffffffu, sx[1], o);
+            if (checker) {
+              sy[0] += __shfl_xor_sync(0xffffffffu, sy[0], o);
+              sy[1] += __shfl_xor_sync(0xffffffffu, sy[1], o);
+            }
+          }
+          if (checker && ((valid[0] && !(isfinite(sx[0]) && isfinite(sy[0]))) ||
+                          (has1 && valid[1] && !(isfinite(sx[1]) && isfinite(sy[1])))))
+            flags |= FLAG_NONFINITE;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (u == 1 && !has1) break;
+            const int rr = u ? r1 : r0;
+            const double mu = ANALYSIS ? sx[u] * inv_n : 0.0;
+            const double rs = valid[u] ? ri[u] : 0.0;
+            double* xr = xs + rr * ld;
+            double* br = bs + rr * ld;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double2 xx = xv[u][h];
+              const double2 yy = yv[u][h];
+              const double s0 = xx.x - mu, s1 = xx.y - mu;
+              *reinterpret_cast<double2*>(xr + 64 * h + 2 * lane) =
+                  valid[u] ? make_double2(s0 * rs, s1 * rs) : make_double2(0.0, 0.0);
+              double2 b;
+              if (pure_d) b = ANALYSIS ? make_double2(yy.x - xx.x, yy.y - xx.y) : yy;
+              else b = ANALYSIS ? make_double2(s0, s1) : xx;
+              if (!valid[u]) b = make_double2(0.0, 0.0);
+              *reinterpret_cast<double2*>(br + 64 * h + 2 * lane) = b;
+            }
+          }
+        }
+      } else
       for (int r0 = tw; r0 < W_RT; r0 += 2 * W_XFORM_WARPS) {
         const int r1 = r0 + W_XFORM_WARPS;
         const bool has1 = r1 < W_RT;
@@ -627,6 +707,7 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
   double* vv = lsm;                               // packed: p(i,c) = c(c+1)/2 + i, i <= c
   double* pcb = vv + levels_vv_doubles(n);        // [2][n] pivot column Gamma[.][k]
   double* qdb = pcb + 2 * n;                      // [2][n] pivot row of V'D: Gamma[k][n + c]
+  double* dinv = qdb + 2 * n;                     // [2]: 1/den of the current / next level
   auto P = [](int i, int c) { return c * (c + 1) / 2 + i; };
   const int n2 = 2 * n;
 
@@ -648,6 +729,7 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
     pcb[i] = gram[i];
     qdb[i] = gram[n + i];
   }
+  if (tid == 0) dinv[0] = 1.0 / (1.0 + gram[0]);
   __syncthreads();
 
   for (int k = 0; k < n; ++k) {
@@ -665,7 +747,7 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
       return;  // uniform: every thread read the same dk
     }
     if (tid == 0 && den_out) den_out[k] = dk;
-    const double inv = 1.0 / dk;
+    const double inv = dinv[cur];  // 1/dk, computed once by the producer of pc[k]
     // V'V: columns c > k, rows i <= c.
 #pragma unroll 1
     for (int c = k + 1 + warp; c < n; c += 32) {
@@ -675,8 +757,12 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
       for (int i = lane; i <= c; i += 32) {
         const double val = col[i] - pc[i] * qc;
         col[i] = val;
-        if (c == k + 1) pcn[i] = val;             // column k+1, rows <= k+1
-        else if (i == k + 1) pcn[c] = val;        // row k+1 = column k+1 by symmetry
+        if (c == k + 1) {                         // column k+1, rows <= k+1
+          pcn[i] = val;
+          if (i == c) dinv[nxt] = 1.0 / (1.0 + val);
+        } else if (i == k + 1) {
+          pcn[c] = val;                           // row k+1 = column k+1 by symmetry
+        }
       }
     }
     // V'D: all rows, all columns (registers).

@@ -239,20 +239,7 @@ def config5(scale_log2: int = 0) -> Problem:
 
 # --------------------------------------------------------------------------
 # Device generation of the config 4/5 shapes (bench), sharded by state rows.
-def shard_rows(n_state: int, world: int, rank: int):
-    """Contiguous state-row shard [lo, hi) of rank `rank`."""
-    base, extra = divmod(n_state, world)
-    lo = rank * base + min(rank, extra)
-    return lo, lo + base + (rank < extra)
-
-
-def obs_slice(indices, lo: int, hi: int):
-    """Observation rows whose (sorted) state index falls in [lo, hi)."""
-    if indices is None:
-        return lo, hi
-    a = int(np.searchsorted(indices, lo, side="left"))
-    b = int(np.searchsorted(indices, hi, side="left"))
-    return a, b
+from .distributed import obs_slice, shard_rows  # noqa: E402  (one definition of the sharding)
 
 
 def device_problem_shard(cfg: int, world: int = 1, rank: int = 0, device=None,
