@@ -11,8 +11,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "enkf_capi.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "enkf_kernels.cuh"),
-                  os.path.join(ROOT, "include", "enkf_b200.h")]
+import glob  # noqa: E402
+
+DEPS = sorted(set(SOURCES + glob.glob(os.path.join(HERE, "csrc", "*.cu*")) +
+                  [os.path.join(ROOT, "include", "enkf_b200.h")]))
 OUT = os.path.join(HERE, "libenkf_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

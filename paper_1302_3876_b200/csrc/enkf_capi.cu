@@ -12,6 +12,7 @@
 
 #include "../../include/enkf_b200.h"
 #include "enkf_kernels.cuh"
+#include "anomaly_i8.cuh"
 
 using namespace enkf;
 
@@ -23,6 +24,9 @@ struct enkf_plan {
   int splits = 1;
   int64_t rows_per_split = 0;
   bool use_ws = true;          // warp-specialised TMA kernels (even N, aligned rows)
+  bool use_128 = true;         // N == 128 specialisation of the Gram pass
+  bool anomaly_i8 = true;      // tensor-core (int8 digit) anomaly update, N == 128
+  int i8_dbg = 0;              // profiling-only role skips (ENKF_I8_DBG)
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
   double* partial = nullptr;  // [splits][n][2n]
@@ -93,6 +97,17 @@ template <bool ANALYSIS>
 cudaError_t launch_gram_ws_t(const enkf_plan* p, const double* X, const double* Y,
                              const int64_t* idx, const double* r, cudaStream_t s) {
   const int n = p->n;
+  if (n == W_TILE && p->use_128) {
+    const int ld = padded_ld(W_TILE);
+    const size_t smem = gram128_smem_bytes(ld);
+    auto kern = gram128_kernel<ANALYSIS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<p->ws_blocks * p->ws_ctas_per_block, W_THREADS, smem, s>>>(
+        X, Y, idx, r, p->n_state, p->n_obs, ld, p->ws_ctas_per_block, p->ws_rows_per_cta, p->partial,
+        p->dstatus);
+    return cudaGetLastError();
+  }
   const int ld = padded_ld(W_TILE);  // operand tiles are 128 wide whatever n is
   const size_t smem = gram_ws_smem_bytes(ld);
   auto kern = gram_ws_kernel<ANALYSIS>;
@@ -176,10 +191,24 @@ cudaError_t launch_rowgemm_ws_t(const enkf_plan* p, const double* P, const doubl
   return cudaGetLastError();
 }
 
+cudaError_t launch_anomaly_i8(const enkf_plan* p, const double* X, const double* T, double* XA,
+                              int64_t n_rows, cudaStream_t s) {
+  const size_t smem = anomaly_i8_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(anomaly_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (n_rows + I8_TILE - 1) / I8_TILE;
+  const int grid = (int)(ntiles < p->num_sms ? ntiles : p->num_sms);
+  if (grid < 1) return cudaSuccess;
+  anomaly_i8_kernel<<<grid, I8_THREADS, smem, s>>>(X, T, XA, n_rows, p->i8_dbg);
+  return cudaGetLastError();
+}
+
 template <int MODE>
 cudaError_t launch_rowgemm(const enkf_plan* p, const double* P, const double* Q, const double* C,
                            const double* r, double* out, int64_t n_rows, cudaStream_t s) {
   const int n = p->n;
+  if (MODE == 0 && p->anomaly_i8 && n == I8_N && aligned16(P) && aligned16(out))
+    return launch_anomaly_i8(p, P, Q, out, n_rows, s);
   if (use_ws(p, P, out) && (C == nullptr || aligned16(C))) {
 #define ENKF_RW(NPV) \
     if (n <= NPV) return launch_rowgemm_ws_t<NPV, MODE>(p, P, Q, C, r, out, n_rows, s);
@@ -424,6 +453,9 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   p->ws_ctas_per_block = cpb;
   p->ws_rows_per_cta = rpc;
   if (const char* env = getenv("ENKF_DISABLE_WS")) p->use_ws = (env[0] == '0');
+  if (const char* env = getenv("ENKF_DISABLE_G128")) p->use_128 = (env[0] == '0');
+  if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
+  if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
 
   const size_t nn = (size_t)n * n;
   size_t partial_elems = (size_t)splits * 2 * nn;

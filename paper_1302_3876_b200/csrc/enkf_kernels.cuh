@@ -650,6 +650,239 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// N == 128 specialisation of the warp-specialised Gram pass (configs 4/5).
+// The two 128-column blocks are pure: block 0 = V'R^-1 V, block 1 = V'R^-1 D.
+// Transform warps only form s = x - mean (in place) and, for block 1,
+// d = y - x (in place): 1-2 FP64 ops per element, 4 rows in flight.  The
+// 1/r_i weight is applied by the DMMA warps to the B fragment they load
+// (k = observation row), so no separate operand buffer exists and the ring is
+// 6 stages deep.  Rationale: transform-side DADDs share the FP64 pipe with
+// DMMA, so their count and dependency depth bound the whole pass.
+constexpr int P_STAGES = 6;
+__host__ __device__ inline size_t gram128_smem_bytes(int ld) {
+  return (size_t)P_STAGES * 2 * W_RT * ld * sizeof(double)
+         + (size_t)P_STAGES * W_RT * (sizeof(double) + sizeof(int))
+         + 3 * P_STAGES * sizeof(uint64_t) + 64;
+}
+
+template <bool ANALYSIS>
+__global__ void __launch_bounds__(W_THREADS, 1)
+gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
+               const int64_t* __restrict__ idx, const double* __restrict__ r,
+               int64_t n_state, int64_t n_obs, int ld, int ctas_per_block,
+               int64_t rows_per_cta, double* __restrict__ partial, DevStatus* __restrict__ status) {
+  constexpr int n = 128;
+  extern __shared__ __align__(128) unsigned char psm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cb = blockIdx.x / ctas_per_block;   // 0: V'V block, 1: V'D block
+  const int part = blockIdx.x % ctas_per_block;
+  const bool dblk = (cb == 1);
+  const bool checker = dblk;
+  const int64_t row_begin = (int64_t)part * rows_per_cta;
+  const int64_t row_end = row_begin + rows_per_cta < n_obs ? row_begin + rows_per_cta : n_obs;
+  const int nstages = row_end > row_begin ? (int)((row_end - row_begin + W_RT - 1) / W_RT) : 0;
+
+  const int stage_elems = W_RT * ld;
+  double* xb = reinterpret_cast<double*>(psm);
+  double* yb = xb + P_STAGES * stage_elems;
+  double* rinv_s = yb + P_STAGES * stage_elems;
+  int* valid_s = reinterpret_cast<int*>(rinv_s + P_STAGES * W_RT);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      (reinterpret_cast<uintptr_t>(valid_s + P_STAGES * W_RT) + 15) & ~uintptr_t(15));
+  uint64_t* load_full = bars;
+  uint64_t* op_full = bars + P_STAGES;
+  uint64_t* op_empty = bars + 2 * P_STAGES;
+
+  if (tid == 0) {
+    for (int i = 0; i < P_STAGES; ++i) {
+      mbar_init(&load_full[i], 1);
+      mbar_init(&op_full[i], 32 * W_XFORM_WARPS);
+      mbar_init(&op_empty[i], 32 * W_MMA_WARPS);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == W_MMA_WARPS) {
+    // ------------------------------------------------------------- loader
+    int flags = 0;
+    auto fetch = [&](int t, bool& valid, int64_t& src, double& rv, int64_t& prev) {
+      const int64_t g = row_begin + (int64_t)t * W_RT + lane;
+      valid = t < nstages && lane < W_RT && g < row_end;
+      src = g;
+      rv = 1.0;
+      prev = -1;
+      if (valid) {
+        rv = r[g];
+        if (ANALYSIS && idx != nullptr) {
+          src = idx[g];
+          if (checker && g > 0) prev = idx[g - 1];
+        }
+      }
+    };
+    bool nvalid;
+    int64_t nsrc, nprev;
+    double nrv;
+    fetch(0, nvalid, nsrc, nrv, nprev);
+    for (int t = 0; t < nstages; ++t) {
+      const int slot = t % P_STAGES;
+      bool valid = nvalid;
+      const int64_t src = nsrc, prev = nprev, g = row_begin + (int64_t)t * W_RT + lane;
+      const double rv = nrv;
+      fetch(t + 1, nvalid, nsrc, nrv, nprev);
+      if (valid) {
+        if (ANALYSIS && idx != nullptr) {
+          if (checker && g > 0 && prev >= src) flags |= FLAG_IDX_ORDER;
+          if (src < 0 || src >= n_state) { flags |= FLAG_IDX_RANGE; valid = false; }
+        }
+        if (checker) {
+          if (!isfinite(rv)) flags |= FLAG_NONFINITE;
+          else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
+        }
+      }
+      if (t >= P_STAGES) mbar_wait(&op_empty[slot], ((t / P_STAGES) - 1) & 1);
+      fence_proxy_async();
+      if (lane < W_RT) {
+        rinv_s[slot * W_RT + lane] = valid ? 1.0 / rv : 0.0;
+        valid_s[slot * W_RT + lane] = valid ? 1 : 0;
+      }
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      const uint32_t row_bytes = (uint32_t)n * 8u;
+      const uint32_t total = (uint32_t)__popc(vmask) * row_bytes * (dblk ? 2u : 1u);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&load_full[slot], total);
+      __syncwarp();
+      if (valid) {
+        bulk_g2s(xb + slot * stage_elems + lane * ld, X + src * (int64_t)n, row_bytes, &load_full[slot]);
+        if (dblk) bulk_g2s(yb + slot * stage_elems + lane * ld, Y + g * (int64_t)n, row_bytes, &load_full[slot]);
+      }
+    }
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 8);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 4);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 2);
+    flags |= __shfl_xor_sync(0xffffffffu, flags, 1);
+    if (lane == 0 && flags) atomicOr(&status->flags, flags);
+    return;
+  }
+
+  if (warp > W_MMA_WARPS) {
+    // ---------------------------------------------------------- transforms
+    const int tw = warp - W_MMA_WARPS - 1;
+    const double inv_n = 1.0 / 128.0;
+    int flags = 0;
+    constexpr int RPI = 4;  // rows in flight per iteration
+    for (int t = 0; t < nstages; ++t) {
+      const int slot = t % P_STAGES;
+      mbar_wait(&load_full[slot], (t / P_STAGES) & 1);
+      double* xs = xb + slot * stage_elems;
+      double* ys = yb + slot * stage_elems;
+      for (int base = tw; base < W_RT; base += RPI * W_XFORM_WARPS) {
+        double2 xv[RPI][2], yv[RPI][2];
+        double sx[RPI], sy[RPI];
+        bool valid[RPI];
+#pragma unroll
+        for (int u = 0; u < RPI; ++u) {
+          const int rr = base + u * W_XFORM_WARPS;
+          const bool inb = rr < W_RT;
+          valid[u] = inb && valid_s[slot * W_RT + rr] != 0;
+          const double* xr = xs + (inb ? rr : 0) * ld;
+          const double* yr = ys + (inb ? rr : 0) * ld;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            xv[u][h] = valid[u] ? *reinterpret_cast<const double2*>(xr + 64 * h + 2 * lane) : make_double2(0.0, 0.0);
+            yv[u][h] = (dblk && valid[u]) ? *reinterpret_cast<const double2*>(yr + 64 * h + 2 * lane)
+                                          : make_double2(0.0, 0.0);
+          }
+          sx[u] = (xv[u][0].x + xv[u][0].y) + (xv[u][1].x + xv[u][1].y);
+          sy[u] = checker ? (yv[u][0].x + yv[u][0].y) + (yv[u][1].x + yv[u][1].y) : 0.0;
+        }
+        if (ANALYSIS || checker) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RPI; ++u) sx[u] += __shfl_xor_sync(0xffffffffu, sx[u], o);
+        }
+        if (checker) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < RPI; ++u) sy[u] += __shfl_xor_sync(0xffffffffu, sy[u], o);
+#pragma unroll
+          for (int u = 0; u < RPI; ++u)
+            if (valid[u] && !(isfinite(sx[u]) && isfinite(sy[u]))) flags |= FLAG_NONFINITE;
+        }
+#pragma unroll
+        for (int u = 0; u < RPI; ++u) {
+          const int rr = base + u * W_XFORM_WARPS;
+          if (rr >= W_RT) break;
+          const double mu = ANALYSIS ? sx[u] * inv_n : 0.0;
+          double* xr = xs + rr * ld;
+          double* yr = ys + rr * ld;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double2 xx = xv[u][h];
+            // s = x - mean (A operand; also the B operand of the V'V block)
+            *reinterpret_cast<double2*>(xr + 64 * h + 2 * lane) =
+                ANALYSIS ? make_double2(xx.x - mu, xx.y - mu) : xx;
+            if (dblk) {
+              const double2 yy = yv[u][h];
+              *reinterpret_cast<double2*>(yr + 64 * h + 2 * lane) =
+                  ANALYSIS ? make_double2(yy.x - xx.x, yy.y - xx.y) : yy;
+            }
+          }
+        }
+      }
+      fence_proxy_async();
+      mbar_arrive(&op_full[slot]);
+    }
+    if (flags) atomicOr(&status->flags, flags);
+    return;
+  }
+
+  // ------------------------------------------------------------------ DMMA
+  const int wm = warp & 1, wn = warp >> 1;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int arow = lane & 3, acol = 64 * wm + (lane >> 2), bcol = 32 * wn + (lane >> 2);
+  for (int t = 0; t < nstages; ++t) {
+    const int slot = t % P_STAGES;
+    mbar_wait(&op_full[slot], (t / P_STAGES) & 1);
+    const double* as = xb + slot * stage_elems;
+    const double* bsm = (dblk ? yb : xb) + slot * stage_elems;
+#pragma unroll
+    for (int ks = 0; ks < W_RT / 4; ++ks) {
+      const int row = 4 * ks + arow;
+      const double ri = rinv_s[slot * W_RT + row];
+      double a[8], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) a[mt] = as[row * ld + acol + 8 * mt];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) b[nt] = bsm[row * ld + bcol + 8 * nt] * ri;
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    }
+    mbar_arrive(&op_empty[slot]);
+  }
+  double* out = partial + (size_t)blockIdx.x * W_TILE * W_TILE;
+#pragma unroll
+  for (int mt = 0; mt < 8; ++mt) {
+    const int i = 64 * wm + 8 * mt + (lane >> 2);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = 32 * wn + 8 * nt + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + i * W_TILE + j) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    }
+  }
+}
+
 // Fixed-order reduction of the warp-specialised partial tiles into the Gram.
 __global__ void gram_ws_reduce(const double* __restrict__ partial, int n, int ctas_per_block,
                                double s_vv, double s_vd, double* __restrict__ gram) {

@@ -309,13 +309,16 @@ def test_tma_kernels_match_generic_kernels(maker, monkeypatch):
     r = torch.from_numpy(p.r).to(dev)
     idx = None if p.indices is None else torch.from_numpy(p.indices).to(dev)
     ns, nobs, n = p.shape
-    plan_ws = _native.Plan(ns, nobs, n, 0)
+    plan_ws = _native.Plan(ns, nobs, n, 0)             # N == 128: gram128 kernel
+    monkeypatch.setenv("ENKF_DISABLE_G128", "1")
+    plan_ws_gen = _native.Plan(ns, nobs, n, 0)         # general warp-specialised kernel
     monkeypatch.setenv("ENKF_DISABLE_WS", "1")
-    plan_gen = _native.Plan(ns, nobs, n, 0)
+    plan_gen = _native.Plan(ns, nobs, n, 0)            # cp.async fallback kernels
     g1, xa1 = _staged_analysis(plan_ws, x, y, idx, r)
     g2, xa2 = _staged_analysis(plan_gen, x, y, idx, r)
-    assert rel_err(g1, g2) <= 1e-13
-    assert rel_err(xa1, xa2) <= 1e-12
+    g3, xa3 = _staged_analysis(plan_ws_gen, x, y, idx, r)
+    assert rel_err(g1, g2) <= 1e-13 and rel_err(g3, g2) <= 1e-13
+    assert rel_err(xa1, xa2) <= 1e-12 and rel_err(xa3, xa2) <= 1e-12
     ref = oracle.analysis_step(p.x, p.perturbed, p.indices, p.r)
     assert rel_err(xa1, ref) <= XA_TOL and rel_err(xa2, ref) <= XA_TOL
 
@@ -349,3 +352,57 @@ def test_solve_ensemble_size_sweep(n, ws, monkeypatch):
         assert rel_err(a.cpu().numpy(), am) <= 1e-10, (n, nobs)
         z_or, _ = oracle.solve_sherman(r, v, d)
         assert rel_err(z.cpu().numpy(), z_or) <= Z_TOL, (n, nobs)
+
+
+@pytest.mark.parametrize("maker", ["config4s8", "config4s4", "config5s6"])
+def test_tensor_core_anomaly_matches_fp64(maker, monkeypatch):
+    """The int8-digit tcgen05 anomaly update (default for N = 128) against the
+    FP64 DMMA kernel and the oracle: fp64-grade (<= 1e-12 relative to max|X^A|)."""
+    import torch
+    p = {"config4s8": lambda: W.config4(8), "config4s4": lambda: W.config4(4),
+         "config5s6": lambda: W.config5(6)}[maker]()
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(p.x).to(dev)
+    y = torch.from_numpy(p.perturbed).to(dev)
+    r = torch.from_numpy(p.r).to(dev)
+    idx = torch.from_numpy(p.indices).to(dev)
+    ns, nobs, n = p.shape
+    assert n == 128
+    plan_tc = _native.Plan(ns, nobs, n, 0)
+    monkeypatch.setenv("ENKF_ANOMALY", "fp64")
+    plan_f64 = _native.Plan(ns, nobs, n, 0)
+    _, xa_tc = _staged_analysis(plan_tc, x, y, idx, r)
+    _, xa_f64 = _staged_analysis(plan_f64, x, y, idx, r)
+    err = rel_err(xa_tc, xa_f64)
+    print(f"{maker}: tcgen05-int8 vs fp64 DMMA {err:.2e}")
+    assert err <= 1e-12
+    ref = oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
+    assert rel_err(xa_tc, ref) <= XA_TOL
+
+
+def test_tensor_core_anomaly_zero_spread_and_nonfinite():
+    import torch
+    dev = torch.device("cuda", 0)
+    n, ns = 128, 1000
+    g = np.random.Generator(np.random.Philox(5))
+    x = np.tile(g.standard_normal(ns)[:, None], (1, n))     # zero spread
+    idx = np.arange(0, ns, 7)
+    y = x[idx] + 0.3
+    xa = P.analysis_step(x, P.ObservationBatch(y=None, perturbed=y, perturbations=None),
+                         P.SelectionOperator.from_indices(idx), np.ones(idx.size))
+    assert np.array_equal(xa, x)                              # exact, as in the reference
+    # a non-finite unobserved row propagates (NaN row), finite rows are unaffected
+    x2 = g.standard_normal((ns, n))
+    x2[3, 5] = np.inf
+    plan = _native.Plan(ns, idx.size, n, 0)
+    xt = torch.from_numpy(x2).to(dev)
+    t = torch.eye(n, dtype=torch.float64, device=dev) + 0.01
+    out = torch.empty_like(xt)
+    s = torch.cuda.current_stream().cuda_stream
+    assert _native.lib().enkf_anomaly_update_f64(plan.handle, xt.data_ptr(), t.data_ptr(), out.data_ptr(), ns, s) == 0
+    o = out.cpu().numpy()
+    assert np.isnan(o[3]).all()
+    mask = np.ones(ns, bool)
+    mask[3] = False
+    ref = x2[mask] @ t.cpu().numpy()
+    assert rel_err(o[mask], ref) <= 1e-12
