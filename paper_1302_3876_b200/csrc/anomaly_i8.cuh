@@ -28,7 +28,8 @@
 namespace enkf {
 
 constexpr int I8_N = 128;         // ensemble size handled by this kernel
-constexpr int I8_TILE = 64;       // X rows per tile
+constexpr int I8_TILE = 32;       // X rows per tile
+constexpr int I8_NBUF = 4;        // pipeline depth (raw X stages and digit buffers)
 constexpr int I8_CHUNK = 16;      // rows per MMA (N of the instruction)
 constexpr int I8_ND = 6;          // byte digits per value
 constexpr int I8_LMAX = 8;        // keep digit pairs with p + q <= 8
@@ -46,8 +47,12 @@ constexpr int I8_ACC0 = I8_ND * 32;
 constexpr int I8_ACCBUF = I8_NLEV * I8_CHUNK;
 
 __host__ __device__ inline size_t anomaly_i8_smem_bytes() {
-  return 1024 /*align slack*/ + 2 * (size_t)I8_XBUF_BYTES + 2 * (size_t)I8_STAGE_BYTES +
-         2 * I8_TILE * sizeof(int) + 256;
+  return 1024 /*align slack*/ + I8_NBUF * ((size_t)I8_XBUF_BYTES + (size_t)I8_STAGE_BYTES) +
+         I8_NBUF * I8_TILE * sizeof(double) + 512;
+}
+// exact int32 -> double: 2^52 + 2^31 trick (one LOP + one DADD)
+__device__ __forceinline__ double i32_to_f64(uint32_t a) {
+  return __hiloint2double(0x43300000, (int)(a ^ 0x80000000u)) - 4503601774854144.0;
 }
 
 // ---- tcgen05 helpers ---------------------------------------------------------
@@ -138,7 +143,6 @@ __device__ __forceinline__ double pow2(int k) {
   if (k < -1022 || k > 1023) return ldexp(1.0, k);
   return __longlong_as_double((long long)(k + 1023) << 52);
 }
-constexpr int I8_NONFINITE = 0x7fff;  // row exponent marker: the row holds inf/nan
 // round(x * 2^s) as int64 for |x 2^s| < 2^51, via the 1.5*2^52 magic constant
 __device__ __forceinline__ long long round_scaled(double x, double scale) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52
@@ -164,19 +168,21 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
                   double* __restrict__ XA, int64_t n_rows, int dbg) {
   // dbg (profiling only): bit0 skip MMAs, bit1 skip slicing, bit2 skip epilogue math/IO
   extern __shared__ __align__(1024) unsigned char i8sm_raw[];
-  unsigned char* i8sm = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(i8sm_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* xdig = i8sm;                                            // [2][6][64][128 B]
-  double* stage = reinterpret_cast<double*>(xdig + 2 * I8_XBUF_BYTES);  // [2][64][128]
-  int* rexp = reinterpret_cast<int*>(stage + 2 * I8_TILE * I8_N);       // [2][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rexp + 2 * I8_TILE);
-  uint64_t* sfull = bars;        // [2] TMA -> slicers/epilogue       (count 1 + tx)
-  uint64_t* sempty = bars + 2;   // [2] slicers+epilogue -> producer  (count slicer+epi threads)
-  uint64_t* xfull = bars + 4;    // [2] slicers -> MMA                (count slicer threads)
-  uint64_t* xempty = bars + 6;   // [2] MMA commit -> slicers         (count 1)
-  uint64_t* afull = bars + 8;    // [2] MMA commit -> epilogue        (count 1)
-  uint64_t* aempty = bars + 10;  // [2] epilogue -> MMA               (count epi threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  // realign by a byte offset (not an integer round trip) so the compiler keeps
+  // the shared address space and emits LDS/STS, not generic LD/ST
+  unsigned char* i8sm = i8sm_raw + ((1024u - (smem_u32(i8sm_raw) & 1023u)) & 1023u);
+  unsigned char* xdig = i8sm;                                                  // [NBUF][6][32][128 B]
+  double* stage = reinterpret_cast<double*>(xdig + I8_NBUF * I8_XBUF_BYTES);  // [NBUF][32][128]
+  // per-row scale factor [NBUF][32] = 2^(e-30) (NaN for non-finite rows)
+  double* rscale = stage + I8_NBUF * I8_TILE * I8_N;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rscale + I8_NBUF * I8_TILE);
+  uint64_t* sfull = bars;                  // [NBUF] TMA -> slicers/epilogue      (count 1 + tx)
+  uint64_t* sempty = bars + I8_NBUF;       // [NBUF] slicers+epilogue -> producer (count slicer+epi)
+  uint64_t* xfull = bars + 2 * I8_NBUF;    // [NBUF] slicers -> MMA               (count slicer threads)
+  uint64_t* xempty = bars + 3 * I8_NBUF;   // [NBUF] MMA commit -> slicers        (count 1)
+  uint64_t* afull = bars + 4 * I8_NBUF;    // [2] MMA commit -> epilogue          (count 1)
+  uint64_t* aempty = bars + 4 * I8_NBUF + 2;  // [2] epilogue -> MMA              (count epi threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * I8_NBUF + 4);
 
   constexpr int EPI0 = I8_SLICE_WARPS;                 // first epilogue warp
   constexpr int MMAW = I8_SLICE_WARPS + I8_EPI_WARPS;  // MMA warp
@@ -186,11 +192,13 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < I8_NBUF; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sempty[i], 32 * (I8_SLICE_WARPS + I8_EPI_WARPS));
       mbar_init(&xfull[i], 32 * I8_SLICE_WARPS);
       mbar_init(&xempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
       mbar_init(&aempty[i], 32 * I8_EPI_WARPS);
     }
@@ -214,9 +222,9 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     // ---- producer: one bulk copy per tile (the tile's rows are contiguous) -----
     if (lane == 0) {
       for (int64_t it = 0; it < my_tiles; ++it) {
-        const int buf = (int)(it & 1);
+        const int buf = (int)(it % I8_NBUF);
         const int64_t tile = blockIdx.x + it * gridDim.x;
-        if (it >= 2) mbar_wait(&sempty[buf], (uint32_t)(((it >> 1) - 1) & 1));
+        if (it >= I8_NBUF) mbar_wait(&sempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
         fence_proxy_async();
         const int64_t g0 = tile * I8_TILE;
         const int rows = (int)(n_rows - g0 < I8_TILE ? n_rows - g0 : I8_TILE);
@@ -245,6 +253,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
       cmax = b > cmax ? b : cmax;
     }
     const int fj = exp_above(cmax);
+    const double fcol = pow2(fj);  // 2^f_j
     if (half == 0) {
       const double cscale = pow2(47 - fj);
 #pragma unroll 1
@@ -266,10 +275,10 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     asm volatile("bar.sync 1, 288;\n" ::: "memory");  // C planes are in TMEM before the first MMA
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      const int buf = (int)(it & 1);
+      const int buf = (int)(it % I8_NBUF);
       const int64_t tile = blockIdx.x + it * gridDim.x;
-      mbar_wait(&sfull[buf], (uint32_t)((it >> 1) & 1));  // raw X of the tile is in smem
-      mbar_wait(&xfull[buf], (uint32_t)((it >> 1) & 1));  // and the slicers' row exponents
+      mbar_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // raw X of the tile is in smem
+      mbar_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // and the slicers' row exponents
       const double* xs = stage + buf * I8_TILE * I8_N;
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
@@ -290,19 +299,23 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(&aempty[ab]);  // accumulators copied out: the MMA may reuse them
+        const double* xrow = xs + r0 * I8_N + j;
+        const double* srow = rscale + buf * I8_TILE + r0;
+        double* orow = XA + g0 * I8_N + j;
+        const int nvalid = (int)(n_rows - g0 < 8 ? n_rows - g0 : 8);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          // levels 2..4 -> hi, 5..8 -> lo (exact int64); X C = 2^(e+f-94) (hi 2^64 + lo 2^32)
-          const long long hi = ((long long)(int)v[0][r] << 16) + ((long long)(int)v[1][r] << 8) +
-                               (long long)(int)v[2][r];
-          const long long lo = ((long long)(int)v[3][r] << 24) + ((long long)(int)v[4][r] << 16) +
-                               ((long long)(int)v[5][r] << 8) + (long long)(int)v[6][r];
-          const int64_t g = g0 + r;
-          if (g < n_rows) {
-            const int e = rexp[buf * I8_TILE + r0 + r];
-            const double xc = fma(i64_to_f64_exact(hi), pow2(e + fj - 30), i64_to_f64_exact(lo) * pow2(e + fj - 62));
-            XA[g * I8_N + j] = (e == I8_NONFINITE) ? __longlong_as_double(0x7ff8000000000000ll)
-                                                    : xs[(r0 + r) * I8_N + j] + xc;
+          // X C = 2^(e+f-94) sum_l acc_l 256^(12-l): levels 2..4 -> hi, 5..8 -> lo,
+          // both exact in fp64 (|hi| < 2^43, |lo| < 2^51), then one rounding
+          const double hi = fma(__int2double_rn((int)v[0][r]), 65536.0,
+                                fma(__int2double_rn((int)v[1][r]), 256.0, __int2double_rn((int)v[2][r])));
+          const double lo = fma(__int2double_rn((int)v[3][r]), 16777216.0,
+                                fma(__int2double_rn((int)v[4][r]), 65536.0,
+                                    fma(__int2double_rn((int)v[5][r]), 256.0, __int2double_rn((int)v[6][r]))));
+          if (r < nvalid) {
+            const double sh = srow[r];  // 2^(e-30)
+            const double xc = fma(hi, sh, lo * (sh * 2.3283064365386963e-10)) * fcol;  // lo 2^(e-62)
+            orow[r * I8_N] = xrow[r * I8_N] + xc;
           }
         }
       }
@@ -315,8 +328,8 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     const uint32_t xbase = smem_u32(xdig);
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      const int buf = (int)(it & 1);
-      mbar_wait(&xfull[buf], (uint32_t)((it >> 1) & 1));
+      const int buf = (int)(it % I8_NBUF);
+      mbar_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));
       tc_fence_after();
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
@@ -354,48 +367,73 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   } else {
     // ---- slicer warps: rows 16w .. 16w+15 of each tile, from the smem stage ----
     for (int64_t it = 0; it < my_tiles; ++it) {
-      const int buf = (int)(it & 1);
-      mbar_wait(&sfull[buf], (uint32_t)((it >> 1) & 1));
-      if (it >= 2) mbar_wait(&xempty[buf], (uint32_t)(((it >> 1) - 1) & 1));
+      const int buf = (int)(it % I8_NBUF);
+      mbar_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));
+      if (it >= I8_NBUF) mbar_wait(&xempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
       unsigned char* planes = xdig + buf * I8_XBUF_BYTES;
       const double* xs = stage + buf * I8_TILE * I8_N;
       if (!(dbg & 2)) {
-#pragma unroll 4
-        for (int rr = 0; rr < I8_TILE / I8_SLICE_WARPS; ++rr) {
-          const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rr;
-          const double2 a0 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane);
-          const double2 a1 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane + 2);
-          const double xv[4] = {a0.x, a0.y, a1.x, a1.y};
-          uint64_t m = 0;
+        constexpr int RG = 8;  // rows in flight: independent load -> max -> split chains
+#pragma unroll 1
+        for (int rb = 0; rb < I8_TILE / I8_SLICE_WARPS; rb += RG) {
+          double xv[RG][4];
+          uint32_t m[RG];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            const uint64_t ab = (uint64_t)__double_as_longlong(xv[b]) & 0x7fffffffffffffffull;
-            m = ab > m ? ab : m;
+          for (int u = 0; u < RG; ++u) {
+            const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
+            const double2 a0 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane);
+            const double2 a1 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane + 2);
+            xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
           }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t other = __shfl_xor_sync(0xffffffffu, m, o);
-            m = other > m ? other : m;
-          }
-          // a non-finite row cannot be split; its digits are zeroed and the
-          // epilogue writes NaN for the whole row (what x T gives in fp64)
-          const bool finite_row = ((m >> 52) & 0x7ff) != 0x7ff;
-          const int e = finite_row ? exp_above(m) : I8_NONFINITE;
-          const double scale = finite_row ? pow2(47 - e) : 0.0;
-          long long v[4];
+          for (int u = 0; u < RG; ++u) {
+            // max exponent of the row from the high words of |x| (exact for the exponent)
+            m[u] = 0;
 #pragma unroll
-          for (int b = 0; b < 4; ++b) v[b] = round_scaled(xv[b], scale);
-          // K-major, 128B-swizzled row r: 16-byte chunk (lane/4) ^ (r%8), word lane%4
-          const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((lane >> 2) ^ (r & 7)) << 4) +
-                                          ((lane & 3) << 2));
-#pragma unroll
-          for (int p = 0; p < I8_ND; ++p) {
-            const int bi = 5 - p;
-            const uint32_t word = byte_of(v[0], bi) | (byte_of(v[1], bi) << 8) | (byte_of(v[2], bi) << 16) |
-                                  (byte_of(v[3], bi) << 24);
-            *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = word;
+            for (int b = 0; b < 4; ++b) m[u] = max(m[u], (uint32_t)__double2hiint(xv[u][b]) & 0x7fffffffu);
           }
-          if (lane == 0) rexp[buf * I8_TILE + r] = e;
+#pragma unroll
+          for (int u = 0; u < RG; ++u) m[u] = __reduce_max_sync(0xffffffffu, m[u]);  // one REDUX per row
+#pragma unroll
+          for (int u = 0; u < RG; ++u) {
+            const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
+            const int bexp = (int)(m[u] >> 20);  // biased exponent of max|x|
+            // a non-finite row cannot be split: zero digits, NaN scale (-> NaN row,
+            // what x T gives in fp64)
+            const bool finite_row = bexp != 0x7ff;
+            const int e = (m[u] == 0) ? 0 : bexp - 1022;  // max|x| < 2^e
+            const double scale = finite_row ? pow2(47 - e) : 0.0;
+            // round(x 2^(47-e)) as a 48-bit integer: the low word of fma(x, s, 1.5 2^52)
+            // is the low word of the integer, the high word is offset by 0x43380000
+            uint32_t vlo[4], vhi[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const double t = fma(xv[u][b], scale, 6755399441055744.0);
+              vlo[b] = (uint32_t)__double2loint(t);
+              vhi[b] = (uint32_t)__double2hiint(t) - 0x43380000u;
+            }
+            // K-major, 128B-swizzled row r: 16-byte chunk (lane/4) ^ (r%8), word lane%4
+            const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((lane >> 2) ^ (r & 7)) << 4) +
+                                            ((lane & 3) << 2));
+            // digit plane p = byte 5-p of the 48-bit values, packed 4 per word
+#pragma unroll
+            for (int p = 0; p < I8_ND; ++p) {
+              const int bi = 5 - p;
+              uint32_t w01, w23;
+              if (bi >= 4) {
+                const uint32_t sel = (uint32_t)(bi - 4) | ((uint32_t)(bi - 4 + 4) << 4);
+                w01 = __byte_perm(vhi[0], vhi[1], sel);
+                w23 = __byte_perm(vhi[2], vhi[3], sel);
+              } else {
+                const uint32_t sel = (uint32_t)bi | ((uint32_t)(bi + 4) << 4);
+                w01 = __byte_perm(vlo[0], vlo[1], sel);
+                w23 = __byte_perm(vlo[2], vlo[3], sel);
+              }
+              *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = __byte_perm(w01, w23, 0x5410);
+            }
+            if (lane == 0)
+              rscale[buf * I8_TILE + r] = finite_row ? pow2(e - 30) : __longlong_as_double(0x7ff8000000000000ll);
+          }
         }
       }
       fence_proxy_async();
