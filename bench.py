@@ -15,8 +15,11 @@ scaling is quoted on; it fits one B200 (X + X^A + Y = 136 GiB).
           max over ranks (strong scaling: the problem is fixed, rows sharded).
   e2e   : the same metric through the public API `analysis_step` with host
           numpy buffers, host->device and device->host copies inside.
-  roofline : the anomaly-update kernel (the dominant one): FP64 DMMA
-          TFLOP/s against the measured FP64 DMMA peak (profiles/).
+  roofline : the anomaly-update kernel (the dominant one).  For n_ens = 128
+          it runs on the tcgen05 int8 tensor cores (exact byte-digit split of
+          the fp64 product) and is HBM-bound: GB/s of X read + X^A written
+          against MEASURED_PEAKS.json.  ENKF_ANOMALY=fp64 selects the FP64
+          DMMA kernel (FP64 TFLOP/s against the measured DMMA peak).
   cpu_baseline : the CPU oracle (oracle/, a numpy/OpenBLAS restatement of the
           reference, which is pure Python) on a bounded row sample of the same
           workload, scaled linearly to the full size (cost is linear in
@@ -267,9 +270,28 @@ def run_ours(args):
     bytes_gram = nobs_loc * (2 * n * 8 + 16)
     try:
         peaks = json.load(open(PEAKS_PATH))
-        hbm_peak = float(peaks["hbm_gbs"])
+        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     except Exception:
-        hbm_peak, peaks = 6650.0, {}
+        hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    anom_gbs = bytes_anom / (t_anom * 1e-3) / 1e9
+    tensor_core = n == 128 and os.environ.get("ENKF_ANOMALY", "i8") != "fp64"
+    if tensor_core:
+        # int8-digit tcgen05 kernel: the FP64 product is exact integer work on
+        # the tensor cores; the kernel is bounded by streaming X in and X^A out
+        roofline = {"bound": "hbm", "kernel": "anomaly_i8_kernel (X^A = X + X C, tcgen05.mma kind::i8 on exact byte digits, TMA-staged)",
+                    "achieved": anom_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": anom_gbs / hbm_peak,
+                    "traffic": None,
+                    "algorithmic": f"read X + write X^A = 2*n_state*n_ens*8 = {bytes_anom:.3e} B per launch",
+                    "peak_source": peak_src,
+                    "fp64_view": {"equivalent_tflops": anom_tflops, "fp64_dmma_peak": FP64_DMMA_PEAK_TFLOPS,
+                                  "frac": anom_tflops / FP64_DMMA_PEAK_TFLOPS}}
+    else:
+        roofline = {"bound": "tensor", "kernel": "rowgemm_ws_kernel (X^A = X T, FP64 DMMA)",
+                    "achieved": anom_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                    "frac": anom_tflops / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
+                    "algorithmic": f"2*n_state*n_ens^2 = {flop_anom:.3e} flop per launch",
+                    "peak_source": "measured FP64 DMMA m8n8k4 issue rate on this pool's B200 (profiles/r01_fp64_probe.json); MEASURED_PEAKS.json has no FP64 entry",
+                    "hbm_view": {"achieved_gbs": anom_gbs, "peak_gbs": hbm_peak, "frac": anom_gbs / hbm_peak}}
     line = {
         "metric": "EnKF analysis steps/sec",
         "value": steps_per_s,
@@ -287,13 +309,7 @@ def run_ours(args):
                    "parallelism": f"row-shard x{world} (NCCL allreduce of the {n}x{2*n} Gram)" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)},
         "kernels_ms": {"gram": t_gram, "allreduce": t_ar, "levels": t_lev, "anomaly": t_anom},
-        "roofline": {"bound": "tensor", "kernel": "rowgemm (anomaly update X^A = X T, FP64 DMMA)",
-                     "achieved": anom_tflops, "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": anom_tflops / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
-                     "algorithmic": f"2*n_state*n_ens^2 = {flop_anom:.3e} flop per launch",
-                     "peak_source": "measured FP64 DMMA m8n8k4 issue rate on this pool's B200 (profiles/r01_fp64_probe.json); MEASURED_PEAKS.json has no FP64 entry",
-                     "hbm_view": {"achieved_gbs": bytes_anom / (t_anom * 1e-3) / 1e9, "peak_gbs": hbm_peak,
-                                  "frac": bytes_anom / (t_anom * 1e-3) / 1e9 / hbm_peak}},
+        "roofline": roofline,
         "gram_kernel": {"tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None,
                         "frac_fp64": (flop_gram / (t_gram * 1e-3) / 1e12) / FP64_DMMA_PEAK_TFLOPS if t_gram > 0 else None,
                         "hbm_gbs": bytes_gram / (t_gram * 1e-3) / 1e9 if t_gram > 0 else None},
