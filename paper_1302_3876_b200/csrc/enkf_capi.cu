@@ -27,6 +27,7 @@ struct enkf_plan {
   bool use_128 = true;         // N == 128 specialisation of the Gram pass
   bool anomaly_i8 = true;      // tensor-core (int8 digit) anomaly update, N == 128
   int i8_dbg = 0;              // profiling-only role skips (ENKF_I8_DBG)
+  bool levels_blocked = true;  // blocked (LB levels per barrier) Sherman-Morrison recursion
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
   double* partial = nullptr;  // [splits][n][2n]
@@ -152,6 +153,13 @@ cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, cons
 
 cudaError_t launch_levels(const enkf_plan* p, const double* gram, double* A, double* T,
                           double* den, double cscale, cudaStream_t s) {
+  if (p->levels_blocked) {
+    const size_t smem = (size_t)levels_blk_smem_doubles(p->n) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(ism_levels_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    ism_levels_blocked_kernel<<<1, 1024, smem, s>>>(gram, p->n, cscale, A, T, den, p->dstatus);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)levels_smem_doubles(p->n) * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(ism_levels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -456,6 +464,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_DISABLE_G128")) p->use_128 = (env[0] == '0');
   if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
+  if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
 
   const size_t nn = (size_t)n * n;
   size_t partial_elems = (size_t)splits * 2 * nn;

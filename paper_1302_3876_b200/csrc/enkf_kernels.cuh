@@ -1062,6 +1062,206 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
 }
 
 // ---------------------------------------------------------------------------
+// Blocked form of the N Sherman-Morrison levels (production): levels are taken
+// LB at a time.  For a block K = {k0..k0+b-1}, applying its b rank-one levels
+// to every later column c equals (Woodbury, W -> W + V_K V_K')
+//     Gamma[:, c] -= Gamma[:, K] (I + Gamma[K, K])^-1 Gamma[K, c],
+// and the sequential den_k of the block are exactly the LDL' pivots of
+// I + Gamma[K, K] (same values, same guard, same 1-based level).  One CTA:
+// gather P = Gamma[:, K], R = Gamma[K, trailing] -> one thread factors the
+// LB x LB block -> Q = M^-1 R column-parallel -> rank-b update of the trailing
+// V'V (packed, smem) and of V'D (registers).  4 barriers per block instead of
+// 1 per level.
+constexpr int LB = 8;
+
+__host__ __device__ inline int64_t levels_blk_smem_doubles(int n) {
+  return levels_vv_doubles(n) + (int64_t)n * n /*VD*/ + (int64_t)LB * n /*PT*/ +
+         (int64_t)LB * 2 * n /*R/Q*/ + (int64_t)LB * LB /*L*/ + 2 * LB /*D, 1/D*/ + n /*colmean*/ + 16;
+}
+
+__global__ void __launch_bounds__(1024, 1)
+ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
+                          double* __restrict__ A, double* __restrict__ T,
+                          double* __restrict__ den_out, DevStatus* __restrict__ status) {
+  extern __shared__ __align__(16) double bsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
+  double* vv = bsm;                                  // packed upper V'V: p(i,c) = c(c+1)/2 + i
+  double* vd = vv + levels_vv_doubles(n);            // [n][n]    V'D (A after the last level)
+  double* PT = vd + (int64_t)n * n;                  // [LB][n]   Gamma[i][k0+j] at PT[j][i]
+  double* RQ = PT + LB * n;                          // [LB][2n]  R, then Q = M^-1 R
+  double* Lm = RQ + LB * 2 * n;                      // [LB][LB]  unit lower factor
+  double* Dm = Lm + LB * LB;                         // [LB]      pivots
+  double* cm = Dm + 2 * LB;                          // [n]       column means (epilogue)
+  int* fail = reinterpret_cast<int*>(cm + n);
+  auto P = [](int i, int c) { return c * (c + 1) / 2 + i; };
+  const int n2 = 2 * n;
+
+  for (int e = tid; e < n * n; e += nthr) {
+    const int i = e / n, c = e - i * n;
+    if (i <= c) vv[P(i, c)] = gram[(int64_t)i * n2 + c];
+    vd[e] = gram[(int64_t)i * n2 + n + c];
+  }
+  if (tid == 0) *fail = 0;
+  __syncthreads();
+
+  for (int k0 = 0; k0 < n; k0 += LB) {
+    const int b = (n - k0) < LB ? (n - k0) : LB;
+    const int c0 = k0 + b;  // first trailing V'V column
+    // ---- 1. gather P = Gamma[:, K], R = Gamma[K, trailing] (M = I + Gamma[K, K] is in PT)
+    for (int e = tid; e < b * n; e += nthr) {
+      const int j = e / n, i = e - j * n, k = k0 + j;
+      PT[j * n + i] = (i <= k) ? vv[P(i, k)] : vv[P(k, i)];
+      if (i >= c0) RQ[j * n2 + i] = vv[P(k, i)];
+      RQ[j * n2 + n + i] = vd[k * n + i];
+    }
+    __syncthreads();
+    // ---- 2. LDL' of M = I + Gamma[K, K] (the block's den_k), one warp in
+    //         registers: lane l holds entries l and l+32 of the row-major 8x8
+    //         block; column j is broadcast by shuffles at step j.  Dm = den,
+    //         Dm[LB + j] = 1/den (one reciprocal per pivot), Lm unit lower.
+    if (warp == 0) {
+      double m[2];
+      int er[2], ec[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        er[h] = e >> 3;
+        ec[h] = e & 7;
+        m[h] = (er[h] < b && ec[h] < b) ? (er[h] == ec[h] ? 1.0 : 0.0) + PT[ec[h] * n + k0 + er[h]] : 0.0;
+      }
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < LB; ++j) {
+        if (j >= b) break;
+        // pivot M[j][j] lives at e = 9j
+        const double d = __shfl_sync(0xffffffffu, (9 * j) < 32 ? m[0] : m[1], (9 * j) & 31);
+        if (fabs(d) < kSingularTol) {
+          if (lane == 0) {
+            if (!(atomicOr(&status->flags, FLAG_SINGULAR) & FLAG_SINGULAR)) {
+              status->level = k0 + j + 1;
+              status->den = d;
+            }
+            *fail = 1;
+          }
+          bad = true;
+          break;
+        }
+        const double dinv = 1.0 / d;
+        if (lane == 0) {
+          Dm[j] = d;
+          Dm[LB + j] = dinv;
+          if (den_out) den_out[k0 + j] = d;
+        }
+        // column j: M[r][j] at e = 8r + j -> lane (8r+j)&31, slot (8r+j)>>5
+        double colr[2], colc[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int er_ = 8 * er[h] + j, ec_ = 8 * ec[h] + j;
+          const double v0 = __shfl_sync(0xffffffffu, m[0], er_ & 31);
+          const double v1 = __shfl_sync(0xffffffffu, m[1], er_ & 31);
+          colr[h] = (er_ >> 5) ? v1 : v0;
+          const double w0 = __shfl_sync(0xffffffffu, m[0], ec_ & 31);
+          const double w1 = __shfl_sync(0xffffffffu, m[1], ec_ & 31);
+          colc[h] = (ec_ >> 5) ? w1 : w0;
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (ec[h] == j && er[h] > j && er[h] < b) Lm[er[h] * LB + j] = m[h] * dinv;
+          if (er[h] > j && ec[h] > j) m[h] -= colr[h] * colc[h] * dinv;
+        }
+      }
+      (void)bad;
+    }
+    __syncthreads();
+    if (*fail) return;  // uniform
+    // ---- 3. Q = M^-1 R, one trailing column per thread
+    const int nv = n - c0;  // trailing V'V columns
+    for (int t = tid; t < nv + n; t += nthr) {
+      const int col = (t < nv) ? (c0 + t) : (n + (t - nv));
+      double y[LB];
+#pragma unroll
+      for (int j = 0; j < LB; ++j) y[j] = (j < b) ? RQ[j * n2 + col] : 0.0;
+#pragma unroll
+      for (int j = 0; j < LB; ++j)
+#pragma unroll
+        for (int m = 0; m < j; ++m) y[j] -= Lm[j * LB + m] * y[m];
+#pragma unroll
+      for (int j = 0; j < LB; ++j) y[j] = (j < b) ? y[j] * Dm[LB + j] : 0.0;
+#pragma unroll
+      for (int j = LB - 1; j >= 0; --j)
+#pragma unroll
+        for (int m = j + 1; m < LB; ++m) y[j] -= Lm[m * LB + j] * y[m];
+#pragma unroll
+      for (int j = 0; j < LB; ++j)
+        if (j < b) RQ[j * n2 + col] = y[j];
+    }
+    __syncthreads();
+    // ---- 4. rank-b update of the trailing V'V (warp per column) and all of V'D
+#pragma unroll 1
+    for (int c = c0 + warp; c < n; c += nwarps) {
+      double q[LB];
+#pragma unroll
+      for (int j = 0; j < LB; ++j) q[j] = (j < b) ? RQ[j * n2 + c] : 0.0;
+      double* col = vv + P(0, c);
+#pragma unroll 1
+      for (int i = lane; i <= c; i += 32) {
+        double acc = col[i];
+#pragma unroll
+        for (int j = 0; j < LB; ++j) acc -= PT[j * n + i] * q[j];  // q[j] = 0 for j >= b
+        col[i] = acc;
+      }
+    }
+    // V'D: 4 x 4 register tiles, P and Q loaded once per tile (rows 4w.., cols 4l..)
+#pragma unroll 1
+    for (int tile = tid; tile < ((n + 3) >> 2) * ((n + 3) >> 2); tile += nthr) {
+      const int nt = (n + 3) >> 2;
+      const int i0 = 4 * (tile / nt), c0v = 4 * (tile - (tile / nt) * nt);
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+          acc[a][bb] = (i0 + a < n && c0v + bb < n) ? vd[(i0 + a) * n + c0v + bb] : 0.0;
+#pragma unroll
+      for (int j = 0; j < LB; ++j) {
+        if (j >= b) break;
+        double pv[4], qv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) pv[a] = (i0 + a < n) ? PT[j * n + i0 + a] : 0.0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) qv[bb] = (c0v + bb < n) ? RQ[j * n2 + n + c0v + bb] : 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) acc[a][bb] -= pv[a] * qv[bb];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+          if (i0 + a < n && c0v + bb < n) vd[(i0 + a) * n + c0v + bb] = acc[a][bb];
+    }
+    __syncthreads();
+  }
+
+  // A = V'Z; T = I + cscale (A - 1 colmean(A)')
+  for (int e = tid; e < n * n; e += nthr) A[e] = vd[e];
+  if (T != nullptr) {
+    for (int c = tid; c < n; c += nthr) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += vd[i * n + c];
+      cm[c] = s / (double)n;
+    }
+    __syncthreads();
+    for (int e = tid; e < n * n; e += nthr) {
+      const int i = e / n, c = e - i * n;
+      T[e] = (i == c ? 1.0 : 0.0) + cscale * (vd[e] - cm[c]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Row-streaming GEMM with the small N x N operand stationary in registers.
 //   MODE 0 (anomaly):  out[i] = P[i] @ Q                (P = X, Q = T)
 //   MODE 1 (Z pass):   out[i] = (C[i] - P[i] @ Q) / r_i  (P = V, C = D, Q = A)
