@@ -30,6 +30,8 @@ struct enkf_plan {
   bool levels_blocked = true;  // blocked (LB levels per barrier) Sherman-Morrison recursion
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
+  int g128_cpb_vv = 1, g128_cpb_vd = 1;     // gram128: CTAs for the V'V / V'D blocks
+  int64_t g128_rows_vv = 0, g128_rows_vd = 0;
   double* partial = nullptr;  // [splits][n][2n]
   double* gram = nullptr;     // [n][2n]
   double* A = nullptr;        // [n][n]
@@ -104,9 +106,9 @@ cudaError_t launch_gram_ws_t(const enkf_plan* p, const double* X, const double* 
     auto kern = gram128_kernel<ANALYSIS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p->ws_blocks * p->ws_ctas_per_block, W_THREADS, smem, s>>>(
-        X, Y, idx, r, p->n_state, p->n_obs, ld, p->ws_ctas_per_block, p->ws_rows_per_cta, p->partial,
-        p->dstatus);
+    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, W_THREADS, smem, s>>>(
+        X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv, p->g128_rows_vv, p->g128_rows_vd,
+        p->partial, p->dstatus);
     return cudaGetLastError();
   }
   const int ld = padded_ld(W_TILE);  // operand tiles are 128 wide whatever n is
@@ -135,8 +137,12 @@ cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, cons
     const double svv = analysis ? 1.0 / (double)(n - 1) : 1.0;
     const double svd = analysis ? 1.0 / std::sqrt((double)(n - 1)) : 1.0;
     const int64_t count = (int64_t)n * 2 * n;
-    gram_ws_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
-                                                                  svv, svd, gram);
+    if (n == W_TILE && p->use_128)
+      gram128_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, p->g128_cpb_vv,
+                                                                     p->g128_cpb_vd, svv, svd, gram);
+    else
+      gram_ws_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
+                                                                    svv, svd, gram);
     return cudaGetLastError();
   }
   const bool vec = (n % 2 == 0) && aligned16(X) && aligned16(Y);
@@ -466,9 +472,32 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
 
+  // gram128 split: the V'V CTAs do 3/4 of the DMMA work of the V'D CTAs (and
+  // lighter transforms), so they get fewer CTAs with more rows each.
+  {
+    double frac = 0.43;
+    if (const char* env = getenv("ENKF_VV_FRAC")) frac = atof(env);
+    int vv = (int)(p->num_sms * frac + 0.5);
+    if (vv < 1) vv = 1;
+    if (vv > p->num_sms - 1) vv = p->num_sms - 1;
+    int vd = p->num_sms - vv;
+    auto rows_for = [&](int ctas) {
+      int64_t rr = (n_obs + ctas - 1) / ctas;
+      rr = (rr + W_RT - 1) / W_RT * W_RT;
+      return rr < W_RT ? (int64_t)W_RT : rr;
+    };
+    p->g128_rows_vv = rows_for(vv);
+    p->g128_rows_vd = rows_for(vd);
+    p->g128_cpb_vv = (int)((n_obs + p->g128_rows_vv - 1) / p->g128_rows_vv);
+    p->g128_cpb_vd = (int)((n_obs + p->g128_rows_vd - 1) / p->g128_rows_vd);
+    if (p->g128_cpb_vv < 1) p->g128_cpb_vv = 1;
+    if (p->g128_cpb_vd < 1) p->g128_cpb_vd = 1;
+  }
   const size_t nn = (size_t)n * n;
   size_t partial_elems = (size_t)splits * 2 * nn;
-  const size_t ws_elems = (size_t)p->ws_blocks * cpb * W_TILE * W_TILE;
+  size_t ws_elems = (size_t)p->ws_blocks * cpb * W_TILE * W_TILE;
+  const size_t g128_elems = (size_t)(p->g128_cpb_vv + p->g128_cpb_vd) * W_TILE * W_TILE;
+  if (g128_elems > ws_elems) ws_elems = g128_elems;
   if (ws_elems > partial_elems) partial_elems = ws_elems;
   e = cudaMalloc(&p->partial, sizeof(double) * partial_elems);
   if (e == cudaSuccess) e = cudaMalloc(&p->gram, sizeof(double) * 2 * nn);

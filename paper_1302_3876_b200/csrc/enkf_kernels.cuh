@@ -669,18 +669,21 @@ __host__ __device__ inline size_t gram128_smem_bytes(int ld) {
          + 3 * P_STAGES * sizeof(uint64_t) + 64;
 }
 
+// The V'V block is symmetric: its CTAs skip the two strictly-lower 64 x 32
+// warp tiles (25 % less DMMA work), and get proportionally more rows each
+// (cpb_vv CTAs for V'V, cpb_vd for V'D, chosen by the host to balance).
 template <bool ANALYSIS>
 __global__ void __launch_bounds__(W_THREADS, 1)
 gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                const int64_t* __restrict__ idx, const double* __restrict__ r,
-               int64_t n_state, int64_t n_obs, int ld, int ctas_per_block,
-               int64_t rows_per_cta, double* __restrict__ partial, DevStatus* __restrict__ status) {
+               int64_t n_state, int64_t n_obs, int ld, int cpb_vv, int64_t rows_vv,
+               int64_t rows_vd, double* __restrict__ partial, DevStatus* __restrict__ status) {
   constexpr int n = 128;
   extern __shared__ __align__(128) unsigned char psm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cb = blockIdx.x / ctas_per_block;   // 0: V'V block, 1: V'D block
-  const int part = blockIdx.x % ctas_per_block;
-  const bool dblk = (cb == 1);
+  const bool dblk = (int)blockIdx.x >= cpb_vv;   // false: V'V block, true: V'D block
+  const int part = dblk ? (int)blockIdx.x - cpb_vv : (int)blockIdx.x;
+  const int64_t rows_per_cta = dblk ? rows_vd : rows_vv;
   const bool checker = dblk;
   const int64_t row_begin = (int64_t)part * rows_per_cta;
   const int64_t row_end = row_begin + rows_per_cta < n_obs ? row_begin + rows_per_cta : n_obs;
@@ -846,6 +849,8 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 
   // ------------------------------------------------------------------ DMMA
   const int wm = warp & 1, wn = warp >> 1;
+  // V'V: rows 64-127 x cols 0-63 lie strictly below the diagonal
+  const bool active = dblk || !(wm == 1 && wn < 2);
   double acc[8][4][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -858,7 +863,7 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     const double* as = xb + slot * stage_elems;
     const double* bsm = (dblk ? yb : xb) + slot * stage_elems;
 #pragma unroll
-    for (int ks = 0; ks < W_RT / 4; ++ks) {
+    for (int ks = 0; ks < (active ? W_RT / 4 : 0); ++ks) {
       const int row = 4 * ks + arow;
       const double ri = rinv_s[slot * W_RT + row];
       double a[8], b[4];
@@ -882,6 +887,28 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
       const int j = 32 * wn + 8 * nt + 2 * (lane & 3);
       *reinterpret_cast<double2*>(out + i * W_TILE + j) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
     }
+  }
+}
+
+
+// Fixed-order reduction for gram128: V'V entries (upper triangle computed,
+// lower mirrored) from the cpb_vv V'V CTAs, V'D entries from the V'D CTAs.
+__global__ void gram128_reduce(const double* __restrict__ partial, int cpb_vv, int cpb_vd,
+                               double s_vv, double s_vd, double* __restrict__ gram) {
+  constexpr int n = 128;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * 2 * n) return;
+  const int i = e / (2 * n), c = e % (2 * n);
+  double s = 0.0;
+  if (c < n) {
+    const int a = i <= c ? i : c, b = i <= c ? c : i;  // upper-triangle source
+    const double* src = partial + a * W_TILE + b;
+    for (int k = 0; k < cpb_vv; ++k) s += src[(size_t)k * W_TILE * W_TILE];
+    gram[e] = s * s_vv;
+  } else {
+    const double* src = partial + (size_t)cpb_vv * W_TILE * W_TILE + i * W_TILE + (c - n);
+    for (int k = 0; k < cpb_vd; ++k) s += src[(size_t)k * W_TILE * W_TILE];
+    gram[e] = s * s_vd;
   }
 }
 

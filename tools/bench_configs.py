@@ -1,0 +1,101 @@
+"""Steps/s of the analysis step at every BASELINE.json configuration (1 GPU),
+device-resident (`enkf_analysis_f64` on CUDA tensors) and through the public
+API with host numpy arrays, next to the CPU oracle on the same inputs.
+
+    python tools/bench_configs.py [--configs 1,2,3,4] [--reps 20]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (CPU baseline: test/bench infrastructure)
+import paper_1302_3876_b200 as P  # noqa: E402
+from paper_1302_3876_b200 import workloads as W  # noqa: E402
+
+
+def problem(cfg):
+    if cfg == 1:
+        return W.config1()
+    if cfg == 2:
+        return W.Config2Cycler().cycle()
+    if cfg == 3:
+        return W.config3()
+    if cfg == 4:
+        return W.config4(0)
+    raise ValueError(cfg)
+
+
+def time_device(p, reps):
+    dev = torch.device("cuda", 0)
+    h = P.SelectionOperator.identity() if p.indices is None else P.SelectionOperator.from_indices(p.indices)
+    x = torch.from_numpy(p.x).to(dev)
+    obs = P.ObservationBatch(y=None, perturbed=torch.from_numpy(p.perturbed).to(dev), perturbations=None)
+    r = torch.from_numpy(p.r).to(dev)
+    for _ in range(3):
+        P.analysis_step(x, obs, h, r)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(reps):
+        P.analysis_step(x, obs, h, r)
+    e1.record()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / reps
+    return e0.elapsed_time(e1) / reps / 1e3, wall
+
+
+def time_host(p, reps):
+    h = P.SelectionOperator.identity() if p.indices is None else P.SelectionOperator.from_indices(p.indices)
+    obs = P.ObservationBatch(y=p.y, perturbed=p.perturbed, perturbations=None)
+    P.analysis_step(p.x, obs, h, p.r)
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        xa = P.analysis_step(p.x, obs, h, p.r)
+    dt = (time.perf_counter() - t0) / reps
+    return dt, xa
+
+
+def time_oracle(p, reps):
+    oracle.analysis_step(p.x, p.perturbed, p.indices, p.r)
+    best = 1e30
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        xa = oracle.analysis_step(p.x, p.perturbed, p.indices, p.r)
+        best = min(best, time.perf_counter() - t0)
+    return best, xa
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--reps", type=int, default=20)
+    a = ap.parse_args()
+    out = {}
+    for cfg in [int(c) for c in a.configs.split(",")]:
+        p = problem(cfg)
+        reps = a.reps if cfg < 4 else 3
+        dev_s, dev_wall = time_device(p, reps)
+        host_s, xa = time_host(p, reps if cfg < 4 else 2)
+        cpu_s, ref = time_oracle(p, 3 if cfg < 4 else 1)
+        err = float(np.abs(xa - ref).max() / np.abs(ref).max())
+        out[f"config{cfg}"] = {
+            "shape": {"n_state": p.shape[0], "n_obs": p.shape[1], "n_ens": p.shape[2]},
+            "device_steps_per_s": 1.0 / dev_s, "device_ms": dev_s * 1e3, "device_wall_ms": dev_wall * 1e3,
+            "host_api_steps_per_s": 1.0 / host_s, "host_api_ms": host_s * 1e3,
+            "cpu_oracle_steps_per_s": 1.0 / cpu_s, "cpu_oracle_ms": cpu_s * 1e3, "cpu_threads": os.cpu_count(),
+            "xa_rel_err_vs_oracle": err,
+        }
+        print(json.dumps({f"config{cfg}": out[f"config{cfg}"]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
