@@ -373,7 +373,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
       unsigned char* planes = xdig + buf * I8_XBUF_BYTES;
       const double* xs = stage + buf * I8_TILE * I8_N;
       if (!(dbg & 2)) {
-        constexpr int RG = 8;  // rows in flight: independent load -> max -> split chains
+        constexpr int RG = (I8_TILE / I8_SLICE_WARPS) < 8 ? (I8_TILE / I8_SLICE_WARPS) : 8;  // rows in flight: independent load -> max -> split chains
 #pragma unroll 1
         for (int rb = 0; rb < I8_TILE / I8_SLICE_WARPS; rb += RG) {
           double xv[RG][4];
@@ -415,22 +415,23 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
             // K-major, 128B-swizzled row r: 16-byte chunk (lane/4) ^ (r%8), word lane%4
             const uint32_t off = (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((lane >> 2) ^ (r & 7)) << 4) +
                                             ((lane & 3) << 2));
-            // digit plane p = byte 5-p of the 48-bit values, packed 4 per word
+            // digit plane p = byte 5-p of the 48-bit values, packed 4 per word.
+            // Two planes per 4 PRMT: A = [v0.bi, v1.bi, v0.bj, v1.bj],
+            // B = [v2.bi, v3.bi, v2.bj, v3.bj] -> plane i = (A,B)[0,1,4,5], j = [2,3,6,7]
+            auto two_planes = [&](uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t bi, uint32_t bj,
+                                  uint32_t& wi, uint32_t& wj) {
+              const uint32_t sel = bi | ((bi + 4u) << 4) | (bj << 8) | ((bj + 4u) << 12);
+              const uint32_t A = __byte_perm(x0, x1, sel);
+              const uint32_t B = __byte_perm(x2, x3, sel);
+              wi = __byte_perm(A, B, 0x5410);
+              wj = __byte_perm(A, B, 0x7632);
+            };
+            uint32_t w[I8_ND];
+            two_planes(vhi[0], vhi[1], vhi[2], vhi[3], 1u, 0u, w[0], w[1]);  // bytes 5, 4
+            two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 3u, 2u, w[2], w[3]);  // bytes 3, 2
+            two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 1u, 0u, w[4], w[5]);  // bytes 1, 0
 #pragma unroll
-            for (int p = 0; p < I8_ND; ++p) {
-              const int bi = 5 - p;
-              uint32_t w01, w23;
-              if (bi >= 4) {
-                const uint32_t sel = (uint32_t)(bi - 4) | ((uint32_t)(bi - 4 + 4) << 4);
-                w01 = __byte_perm(vhi[0], vhi[1], sel);
-                w23 = __byte_perm(vhi[2], vhi[3], sel);
-              } else {
-                const uint32_t sel = (uint32_t)bi | ((uint32_t)(bi + 4) << 4);
-                w01 = __byte_perm(vlo[0], vlo[1], sel);
-                w23 = __byte_perm(vlo[2], vlo[3], sel);
-              }
-              *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = __byte_perm(w01, w23, 0x5410);
-            }
+            for (int p = 0; p < I8_ND; ++p) *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = w[p];
             if (lane == 0)
               rscale[buf * I8_TILE + r] = finite_row ? pow2(e - 30) : __longlong_as_double(0x7ff8000000000000ll);
           }
