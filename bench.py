@@ -223,7 +223,9 @@ def run_ours(args):
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
         ms = float(mt.item())
 
-    # --- e2e through the public API with host buffers (rank-local problem)
+    # --- e2e with host buffers, copies inside the timed region.  One GPU: the
+    # public drop-in `analysis_step(numpy arrays)`; N GPUs: the public sharded
+    # API (`distributed.ShardedAnalysis`) fed from each rank's host shard.
     e2e = None
     if not args.no_e2e:
         import paper_1302_3876_b200 as P
@@ -236,26 +238,42 @@ def run_ours(args):
         del x, xa, yv
         torch.cuda.synchronize(dev)
         torch.cuda.empty_cache()
-        h = P.SelectionOperator.from_indices(idx_loc)
-        obs = P.ObservationBatch(y=None, perturbed=y_h.numpy(), perturbations=None)
-        xnp = x_h.numpy()
-        out = P.analysis_step(xnp, obs, h, r_h)  # warm (allocates the plan's staging)
-        del out
+        if world == 1:
+            h = P.SelectionOperator.from_indices(idx_loc)
+            obs = P.ObservationBatch(y=None, perturbed=y_h.numpy(), perturbations=None)
+            xnp = x_h.numpy()
+
+            def e2e_step():
+                out = P.analysis_step(xnp, obs, h, r_h)  # numpy in, numpy out
+                return out
+        else:
+            out_h = torch.empty_like(x_h, pin_memory=True)
+            r_d = torch.from_numpy(r_h).to(dev)
+            idx_d = torch.from_numpy(idx_loc).to(dev)
+
+            def e2e_step():
+                xd = x_h.to(dev, non_blocking=True)
+                yd = y_h.to(dev, non_blocking=True)
+                runner.step(xd, yd, idx_d, r_d, xd)  # in place; raises on any rank's error
+                out_h.copy_(xd)
+                torch.cuda.synchronize(dev)
+                return out_h
+        e2e_step()  # warm (plans, staging)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            out = P.analysis_step(xnp, obs, h, r_h)
-            del out
+            e2e_step()
         el = time.perf_counter() - t0
         if world > 1:
             et = torch.tensor([el], dtype=torch.float64, device=dev)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
             el = float(et.item())
         e2e = {"value": args.e2e_steps / el, "unit": "steps/s",
-               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes + idx_loc.nbytes),
-               "d2h_bytes_per_step": int(x_h.numel() * 8), "steps": args.e2e_steps,
-               "api": "paper_1302_3876_b200.analysis_step(numpy host arrays) -> enkf_analysis_host_f64"}
+               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes + idx_loc.nbytes) * world,
+               "d2h_bytes_per_step": int(x_h.numel() * 8) * world, "steps": args.e2e_steps,
+               "api": ("paper_1302_3876_b200.analysis_step(numpy host arrays) -> enkf_analysis_host_f64" if world == 1
+                       else "paper_1302_3876_b200.distributed.ShardedAnalysis.step from pinned host shards")}
 
     if rank != 0:
         if world > 1:
