@@ -663,6 +663,7 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 // 6 stages deep.  Rationale: transform-side DADDs share the FP64 pipe with
 // DMMA, so their count and dependency depth bound the whole pass.
 constexpr int P_STAGES = 6;
+constexpr int P_XFORM = 4;  // gram128: transform warps 8..11 (warp 8 also loads)
 __host__ __device__ inline size_t gram128_smem_bytes(int ld) {
   return (size_t)P_STAGES * 2 * W_RT * ld * sizeof(double)
          + (size_t)P_STAGES * W_RT * (sizeof(double) + sizeof(int))
@@ -703,16 +704,25 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   if (tid == 0) {
     for (int i = 0; i < P_STAGES; ++i) {
       mbar_init(&load_full[i], 1);
-      mbar_init(&op_full[i], 32 * W_XFORM_WARPS);
+      mbar_init(&op_full[i], 32 * P_XFORM);
       mbar_init(&op_empty[i], 32 * W_MMA_WARPS);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == W_MMA_WARPS) {
-    // ------------------------------------------------------------- loader
+  if (warp >= W_MMA_WARPS) {
+    // ------------------------------------------------- transforms (+ loader)
+    // Warps 8..11 transform rows tw, tw+4, tw+8, tw+12 of each stage; warp 8
+    // also streams the rows in (idx/r prefetched one stage ahead, one bulk TMA
+    // copy per gathered X row and per Y row), S-1 stages ahead of the DMMA warps.
+    const int tw = warp - W_MMA_WARPS;
+    const double inv_n = 1.0 / 128.0;
     int flags = 0;
+    // loader state (warp 8 only)
+    bool nvalid = false;
+    int64_t nsrc = 0, nprev = -1;
+    double nrv = 1.0;
     auto fetch = [&](int t, bool& valid, int64_t& src, double& rv, int64_t& prev) {
       const int64_t g = row_begin + (int64_t)t * W_RT + lane;
       valid = t < nstages && lane < W_RT && g < row_end;
@@ -727,16 +737,12 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
         }
       }
     };
-    bool nvalid;
-    int64_t nsrc, nprev;
-    double nrv;
-    fetch(0, nvalid, nsrc, nrv, nprev);
-    for (int t = 0; t < nstages; ++t) {
-      const int slot = t % P_STAGES;
+    auto issue = [&](int u) {  // stream stage u (its slot's previous stage already consumed)
+      const int slot = u % P_STAGES;
       bool valid = nvalid;
-      const int64_t src = nsrc, prev = nprev, g = row_begin + (int64_t)t * W_RT + lane;
+      const int64_t src = nsrc, prev = nprev, g = row_begin + (int64_t)u * W_RT + lane;
       const double rv = nrv;
-      fetch(t + 1, nvalid, nsrc, nrv, nprev);
+      fetch(u + 1, nvalid, nsrc, nrv, nprev);
       if (valid) {
         if (ANALYSIS && idx != nullptr) {
           if (checker && g > 0 && prev >= src) flags |= FLAG_IDX_ORDER;
@@ -747,7 +753,6 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
           else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
         }
       }
-      if (t >= P_STAGES) mbar_wait(&op_empty[slot], ((t / P_STAGES) - 1) & 1);
       fence_proxy_async();
       if (lane < W_RT) {
         rinv_s[slot * W_RT + lane] = valid ? 1.0 / rv : 0.0;
@@ -763,38 +768,28 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
         bulk_g2s(xb + slot * stage_elems + lane * ld, X + src * (int64_t)n, row_bytes, &load_full[slot]);
         if (dblk) bulk_g2s(yb + slot * stage_elems + lane * ld, Y + g * (int64_t)n, row_bytes, &load_full[slot]);
       }
+    };
+    if (tw == 0) {
+      fetch(0, nvalid, nsrc, nrv, nprev);
+      for (int u = 0; u < P_STAGES - 1 && u < nstages; ++u) issue(u);
     }
-    flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
-    flags |= __shfl_xor_sync(0xffffffffu, flags, 8);
-    flags |= __shfl_xor_sync(0xffffffffu, flags, 4);
-    flags |= __shfl_xor_sync(0xffffffffu, flags, 2);
-    flags |= __shfl_xor_sync(0xffffffffu, flags, 1);
-    if (lane == 0 && flags) atomicOr(&status->flags, flags);
-    return;
-  }
-
-  if (warp > W_MMA_WARPS) {
-    // ---------------------------------------------------------- transforms
-    const int tw = warp - W_MMA_WARPS - 1;
-    const double inv_n = 1.0 / 128.0;
-    int flags = 0;
-    constexpr int RPI = 4;  // rows in flight per iteration
+    constexpr int RPI = W_RT / P_XFORM;  // 4 rows per warp per stage, all in flight
     for (int t = 0; t < nstages; ++t) {
       const int slot = t % P_STAGES;
       mbar_wait(&load_full[slot], (t / P_STAGES) & 1);
       double* xs = xb + slot * stage_elems;
       double* ys = yb + slot * stage_elems;
-      for (int base = tw; base < W_RT; base += RPI * W_XFORM_WARPS) {
+      {
+        const int base = tw;
         double2 xv[RPI][2], yv[RPI][2];
         double sx[RPI], sy[RPI];
         bool valid[RPI];
 #pragma unroll
         for (int u = 0; u < RPI; ++u) {
-          const int rr = base + u * W_XFORM_WARPS;
-          const bool inb = rr < W_RT;
-          valid[u] = inb && valid_s[slot * W_RT + rr] != 0;
-          const double* xr = xs + (inb ? rr : 0) * ld;
-          const double* yr = ys + (inb ? rr : 0) * ld;
+          const int rr = base + u * P_XFORM;
+          valid[u] = valid_s[slot * W_RT + rr] != 0;
+          const double* xr = xs + rr * ld;
+          const double* yr = ys + rr * ld;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             xv[u][h] = valid[u] ? *reinterpret_cast<const double2*>(xr + 64 * h + 2 * lane) : make_double2(0.0, 0.0);
@@ -821,15 +816,13 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
         }
 #pragma unroll
         for (int u = 0; u < RPI; ++u) {
-          const int rr = base + u * W_XFORM_WARPS;
-          if (rr >= W_RT) break;
+          const int rr = base + u * P_XFORM;
           const double mu = ANALYSIS ? sx[u] * inv_n : 0.0;
           double* xr = xs + rr * ld;
           double* yr = ys + rr * ld;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const double2 xx = xv[u][h];
-            // s = x - mean (A operand; also the B operand of the V'V block)
             *reinterpret_cast<double2*>(xr + 64 * h + 2 * lane) =
                 ANALYSIS ? make_double2(xx.x - mu, xx.y - mu) : xx;
             if (dblk) {
@@ -842,12 +835,26 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
       }
       fence_proxy_async();
       mbar_arrive(&op_full[slot]);
+      if (tw == 0) {
+        const int u = t + P_STAGES - 1;  // reuses the slot of stage t-1
+        if (u < nstages) {
+          if (t >= 1) mbar_wait(&op_empty[(t - 1) % P_STAGES], ((t - 1) / P_STAGES) & 1);
+          issue(u);
+        }
+      }
+    }
+    if (tw == 0) {
+      flags |= __shfl_xor_sync(0xffffffffu, flags, 16);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, 8);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, 4);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, 2);
+      flags |= __shfl_xor_sync(0xffffffffu, flags, 1);
     }
     if (flags) atomicOr(&status->flags, flags);
     return;
   }
 
-  // ------------------------------------------------------------------ DMMA
+// ------------------------------------------------------------------ DMMA
   const int wm = warp & 1, wn = warp >> 1;
   // V'V: rows 64-127 x cols 0-63 lie strictly below the diagonal
   const bool active = dblk || !(wm == 1 && wn < 2);
