@@ -17,6 +17,9 @@
  *   enkf_anomaly_update_f64 enkf.py:192        x + s @ A  (A = v' z), as X @ T
  *   enkf_member_deviations_f64 enkf.py:82-92   member_deviations
  *   enkf_innovations_f64    enkf.py:114-120    innovations (Y - H X)
+ *   enkf_analysis_localized_f64        enkf.py:193-199  analysis_step(..., localization=delta)
+ *   enkf_analysis_localized_cyclic_f64 enkf.py:193-199 with delta = influence_matrix_cyclic
+ *                           (enkf.py:138-164) evaluated on the fly (matrix-free)
  *
  * Layouts (all fp64 row-major, the reference's C-order arrays):
  *   X, XA : [n_state][n_ens]      Y, D, V, Z : [n_obs][n_ens]
@@ -99,6 +102,20 @@ int32_t enkf_plan_reset_status(enkf_plan* plan, void* stream);
 int32_t enkf_analysis_host_f64(enkf_plan* plan, const double* X_h, const double* Y_h,
                                const int64_t* idx_h, const double* r_h, double* XA_h,
                                enkf_status* status);
+
+/* Localized analysis (enkf.py:193-199): XA = X + (delta o (S V')) Z, Z from the
+ * ISM solve of (r, V, D).  delta: device fp64 [n_state][n_obs] (row-major, the
+ * reference's (nstate, nobs) influence matrix).  S V' is never materialised.
+ * Same status semantics as enkf_analysis_f64; synchronous. */
+int32_t enkf_analysis_localized_f64(enkf_plan* plan, const double* X, const double* Y,
+                                    const int64_t* idx, const double* r, const double* delta,
+                                    double* XA, void* stream, enkf_status* status);
+/* Matrix-free variant: delta_ij = exp(-d(i, p_j) / scale), d the cyclic distance
+ * min(|i - p_j|, n_state - |i - p_j|), p_j = idx[j] (or j when idx is NULL), as
+ * influence_matrix_cyclic (enkf.py:138-164).  scale <= 0 -> INVALID_ARGUMENT. */
+int32_t enkf_analysis_localized_cyclic_f64(enkf_plan* plan, const double* X, const double* Y,
+                                           const int64_t* idx, const double* r, double scale,
+                                           double* XA, void* stream, enkf_status* status);
 
 /* --- staged form (multi-GPU: partial Gram -> allreduce by the caller -> levels) --- */
 

@@ -19,7 +19,9 @@ from .enkf_oracle import (  # noqa: F401
     OracleSingularUpdate,
     analysis_step,
     analysis_step_chunked,
+    analysis_step_localized,
     apply_selection,
+    influence_matrix_cyclic,
     innovations,
     long_op_count,
     member_deviations,

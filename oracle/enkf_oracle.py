@@ -191,3 +191,35 @@ def analysis_step_chunked(x, perturbed, indices, r, rows_per_chunk=1 << 18):
         blk = x[lo:lo + rows_per_chunk]
         out[lo:lo + rows_per_chunk] = blk + member_deviations(blk) @ a
     return out
+
+
+def influence_matrix_cyclic(nstate, indices, scale=None):
+    """enkf.py:138-164: exp(-d(i, p_j) / scale), cyclic index distance;
+    ``indices`` None means the identity operator (p_j = j)."""
+    if scale is None:
+        scale = float(nstate)
+    if scale <= 0:
+        raise ValueError("influence scale must be positive")
+    obs_idx = np.arange(nstate) if indices is None else np.asarray(indices)
+    if indices is not None and obs_idx[-1] >= nstate:
+        raise ValueError("observation index out of range")
+    i = np.arange(nstate)[:, None]
+    raw = np.abs(i - obs_idx[None, :])
+    dist = np.minimum(raw, nstate - raw)
+    return np.exp(-dist / scale)
+
+
+def analysis_step_localized(x, perturbed, indices, r, delta):
+    """enkf.py:187-199 (localized branch): X + (Delta o (S V')) Z."""
+    x = np.asarray(x, dtype=float)
+    if x.ndim != 2 or x.shape[1] < 2:
+        raise ValueError("analysis needs at least 2 ensemble members")
+    s = member_deviations(x)
+    v = apply_selection(indices, s)
+    d = innovations(perturbed, indices, x)
+    z, _ = solve_sherman(r, v, d)
+    delta = np.asarray(delta, dtype=float)
+    if delta.shape != (x.shape[0], v.shape[0]):
+        raise ValueError(f"influence matrix shape {delta.shape} does not match "
+                         f"(nstate, nobs) = ({x.shape[0]}, {v.shape[0]})")
+    return x + (delta * (s @ v.T)) @ z

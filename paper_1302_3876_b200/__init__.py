@@ -4,14 +4,17 @@ Drop-in for the hot path of the reference package `enkfkit`: the names below
 keep the reference's signatures and semantics (reference __init__.py:11-84),
 while the arithmetic runs in hand-written sm_100a CUDA (libenkf_b200.so,
 C ABI in include/enkf_b200.h).  Out-of-scope reference components (models,
-twin-experiment harness, Cholesky/SVD baselines, localization, CLI) are not
-provided.
+twin-experiment harness, Cholesky/SVD baselines, CLI) are not provided;
+localized analysis (enkf.py:193-199) runs on the GPU, with the cyclic
+influence matrix evaluated on the fly.
 """
 
 from .enkf import (
+    CyclicInfluence,
     ObservationBatch,
     SelectionOperator,
     analysis_step,
+    influence_matrix_cyclic,
     innovations,
     member_deviations,
 )
@@ -37,6 +40,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "ConfigError",
+    "CyclicInfluence",
     "DivergenceError",
     "GROUP_LEVELS",
     "NotPositiveDefiniteError",
@@ -48,6 +52,7 @@ __all__ = [
     "SolverChoice",
     "SolverResult",
     "analysis_step",
+    "influence_matrix_cyclic",
     "innovations",
     "level_blocks",
     "long_op_count",

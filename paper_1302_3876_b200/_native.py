@@ -13,7 +13,10 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libenkf_b200.so")
+# ENKF_LIB_VARIANT=<name> loads libenkf_b200_<name>.so (in-tree kernel variants
+# built by tools/build_variant.py for A/B timing); the default is the product build.
+_VARIANT = os.environ.get("ENKF_LIB_VARIANT", "")
+LIB_PATH = os.path.join(_HERE, f"libenkf_b200_{_VARIANT}.so" if _VARIANT else "libenkf_b200.so")
 
 ENKF_OK = 0
 ENKF_INVALID_ARGUMENT = 1
@@ -55,6 +58,8 @@ PROTOTYPES = {
     "enkf_ism_solve_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _st]),
     "enkf_member_deviations_f64": (_i32, [_vp, _vp, _i64, _i64, _vp]),
     "enkf_innovations_f64": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    "enkf_analysis_localized_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _st]),
+    "enkf_analysis_localized_cyclic_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _st]),
 }
 
 _lib = None

@@ -34,8 +34,17 @@ constexpr int I8_CHUNK = 16;      // rows per MMA (N of the instruction)
 constexpr int I8_ND = 6;          // byte digits per value
 constexpr int I8_LMAX = 8;        // keep digit pairs with p + q <= 8
 constexpr int I8_NLEV = I8_LMAX - 1;  // levels 2..8
-constexpr int I8_SLICE_WARPS = 4;
-constexpr int I8_EPI_WARPS = 8;   // two per TMEM lane quadrant, each half of a chunk's rows
+#ifndef I8_SW
+#define I8_SW 4
+#endif
+#ifndef I8_EW
+#define I8_EW 8
+#endif
+constexpr int I8_SLICE_WARPS = I8_SW;
+constexpr int I8_EPI_WARPS = I8_EW;   // I8_EW/4 per TMEM lane quadrant, each a slice of a chunk's rows
+constexpr int I8_EPI_GROUPS = I8_EPI_WARPS / 4;
+constexpr int I8_RPT = I8_CHUNK / I8_EPI_GROUPS;  // chunk rows per epilogue thread
+static_assert(I8_RPT == 4 || I8_RPT == 8, "epilogue rows per thread");
 constexpr int I8_THREADS = (I8_SLICE_WARPS + I8_EPI_WARPS + 2) * 32;  // + MMA warp + TMA warp
 constexpr int I8_STAGE_BYTES = I8_TILE * I8_N * 8;     // raw X tile (64 KiB)
 constexpr int I8_PLANE_BYTES = I8_TILE * 128;          // 8 KiB per digit plane
@@ -54,6 +63,45 @@ __host__ __device__ inline size_t anomaly_i8_smem_bytes() {
 __device__ __forceinline__ double i32_to_f64(uint32_t a) {
   return __hiloint2double(0x43300000, (int)(a ^ 0x80000000u)) - 4503601774854144.0;
 }
+
+// K order of the digit planes: word w of a plane row holds k = 2w, 2w+1, 64+2w,
+// 65+2w (bytes 0..3).  Any permutation of k applied to both operands leaves the
+// products unchanged; this one lets a slicer lane fetch its 4 values with two
+// contiguous 512-byte LDS.128 rows (no bank conflicts).
+__host__ __device__ __forceinline__ int i8_kperm(int w, int b) { return (b < 2 ? 2 * w + b : 64 + 2 * w + b - 2); }
+
+#ifndef I8_WAIT_HINT
+#define I8_WAIT_HINT 1
+#endif
+#ifndef I8_WARP_ARRIVE
+#define I8_WARP_ARRIVE 0
+#endif
+// mbarrier wait used by this kernel (variant selectable at compile time)
+__device__ __forceinline__ void i8_wait(uint64_t* bar, uint32_t parity) {
+#if I8_WAIT_HINT
+  mbar_wait(bar, parity);
+#else
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+#endif
+}
+// one arrival per warp (barrier counts are in warps) or per thread
+__device__ __forceinline__ void i8_arrive(uint64_t* bar) {
+#if I8_WARP_ARRIVE
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+#else
+  mbar_arrive(bar);
+#endif
+}
+constexpr int I8_ARRIVE_UNIT = I8_WARP_ARRIVE ? 1 : 32;
 
 // ---- tcgen05 helpers ---------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -116,6 +164,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
                : "r"(taddr));
 }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+template <int R>
+__device__ __forceinline__ void tmem_ldr(uint32_t taddr, uint32_t (&v)[R]) {
+  if constexpr (R == 8) tmem_ld8(taddr, v); else tmem_ld4(taddr, v);
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
@@ -163,6 +220,19 @@ __device__ __forceinline__ uint32_t byte_of(long long v, int b) { return (uint32
 //   slicers  : stage[buf] -> 6 byte-digit planes (K-major, 128B swizzle) + row exponents
 //   MMA      : 4 chunks x 26 digit pairs x 4 k-steps of tcgen05.mma kind::i8
 //   epilogue : TMEM -> exact int64 recombination -> fp64, + X (from stage[buf]) -> X^A
+// Profiling-only trace (CTA 0): [tile][event] globaltimer stamps, events:
+// 0 TMA issued, 1 stage landed (slicer view), 2 slicing done, 3 MMA issue start,
+// 4 MMA issue end, 5 epilogue first chunk ready, 6 epilogue done.
+constexpr int I8_TRACE_TILES = 256;
+__device__ unsigned long long g_i8_trace[I8_TRACE_TILES][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define I8_TRACE(it, ev) \
+  do { if ((dbg & 8) && blockIdx.x == 0 && (it) < I8_TRACE_TILES) g_i8_trace[(it)][(ev)] = gtime(); } while (0)
+
 __global__ void __launch_bounds__(I8_THREADS, 1)
 anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* = T */,
                   double* __restrict__ XA, int64_t n_rows, int dbg) {
@@ -194,13 +264,13 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   if (tid == 0) {
     for (int i = 0; i < I8_NBUF; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 32 * (I8_SLICE_WARPS + I8_EPI_WARPS));
-      mbar_init(&xfull[i], 32 * I8_SLICE_WARPS);
+      mbar_init(&sempty[i], I8_ARRIVE_UNIT * (I8_SLICE_WARPS + I8_EPI_WARPS));
+      mbar_init(&xfull[i], I8_ARRIVE_UNIT * I8_SLICE_WARPS);
       mbar_init(&xempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
-      mbar_init(&aempty[i], 32 * I8_EPI_WARPS);
+      mbar_init(&aempty[i], I8_ARRIVE_UNIT * I8_EPI_WARPS);
     }
     fence_mbar_init();
   }
@@ -224,12 +294,13 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
       for (int64_t it = 0; it < my_tiles; ++it) {
         const int buf = (int)(it % I8_NBUF);
         const int64_t tile = blockIdx.x + it * gridDim.x;
-        if (it >= I8_NBUF) mbar_wait(&sempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
+        if (it >= I8_NBUF) i8_wait(&sempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
         fence_proxy_async();
         const int64_t g0 = tile * I8_TILE;
         const int rows = (int)(n_rows - g0 < I8_TILE ? n_rows - g0 : I8_TILE);
         const uint32_t bytes = (uint32_t)rows * I8_N * 8u;
         mbar_arrive_expect_tx(&sfull[buf], bytes);
+        I8_TRACE(it, 0);
         double* dst = stage + buf * I8_TILE * I8_N;
         const double* src = X + g0 * I8_N;
         for (uint32_t off = 0; off < bytes; off += 16384u) {
@@ -242,7 +313,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   } else if (warp >= EPI0 && warp < MMAW) {
     // ---- epilogue warps: thread = output column j = TMEM lane ------------------
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
-    const int half = (warp - EPI0) >> 2;  // which 8 rows of each 16-row chunk
+    const int half = (warp - EPI0) >> 2;  // which I8_RPT rows of each 16-row chunk
     const int j = 32 * quad + lane;
     // C^T digit planes into TMEM (A operand), column scale f_j
     // C = T - I (T = I + (I - 11'/N) A / sqrt(N-1) from the levels kernel)
@@ -263,7 +334,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
           uint32_t word = 0;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            const long long v = round_scaled(cval(4 * w + b), cscale);
+            const long long v = round_scaled(cval(i8_kperm(w, b)), cscale);
             word |= byte_of(v, 5 - p) << (8 * b);
           }
           tmem_st1(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(32 * p + w), word);
@@ -272,39 +343,40 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
       tmem_st_wait();
     }
     tc_fence_before();
-    asm volatile("bar.sync 1, 288;\n" ::: "memory");  // C planes are in TMEM before the first MMA
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (I8_EPI_WARPS + 1)) : "memory");  // C planes in TMEM before the first MMA
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
       const int64_t tile = blockIdx.x + it * gridDim.x;
-      mbar_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // raw X of the tile is in smem
-      mbar_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // and the slicers' row exponents
+      i8_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // raw X of the tile is in smem
+      i8_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // and the slicers' row exponents
       const double* xs = stage + buf * I8_TILE * I8_N;
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
-        const int r0 = c * I8_CHUNK + 8 * half;  // first tile row of this thread's 8
+        const int r0 = c * I8_CHUNK + I8_RPT * half;  // first tile row of this thread's I8_RPT
         const int64_t g0 = tile * I8_TILE + r0;
-        mbar_wait(&afull[ab], (uint32_t)((chunk_ctr >> 1) & 1));
+        i8_wait(&afull[ab], (uint32_t)((chunk_ctr >> 1) & 1));
         tc_fence_after();
+        if (c == 0 && warp == EPI0 && lane == 0) I8_TRACE(it, 5);
         if (dbg & 4) {
           tc_fence_before();
-          mbar_arrive(&aempty[ab]);
+          i8_arrive(&aempty[ab]);
           continue;
         }
         const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) +
-                               (uint32_t)(I8_ACC0 + ab * I8_ACCBUF + 8 * half);
-        uint32_t v[I8_NLEV][8];
+                               (uint32_t)(I8_ACC0 + ab * I8_ACCBUF + I8_RPT * half);
+        uint32_t v[I8_NLEV][I8_RPT];
 #pragma unroll
-        for (int l = 0; l < I8_NLEV; ++l) tmem_ld8(tbase + (uint32_t)(l * I8_CHUNK), v[l]);
+        for (int l = 0; l < I8_NLEV; ++l) tmem_ldr<I8_RPT>(tbase + (uint32_t)(l * I8_CHUNK), v[l]);
         tmem_ld_wait();
         tc_fence_before();
-        mbar_arrive(&aempty[ab]);  // accumulators copied out: the MMA may reuse them
+        i8_arrive(&aempty[ab]);  // accumulators copied out: the MMA may reuse them
         const double* xrow = xs + r0 * I8_N + j;
         const double* srow = rscale + buf * I8_TILE + r0;
         double* orow = XA + g0 * I8_N + j;
-        const int nvalid = (int)(n_rows - g0 < 8 ? n_rows - g0 : 8);
+        const int nvalid = (int)(n_rows - g0 < I8_RPT ? n_rows - g0 : I8_RPT);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < I8_RPT; ++r) {
           // X C = 2^(e+f-94) sum_l acc_l 256^(12-l): levels 2..4 -> hi, 5..8 -> lo,
           // both exact in fp64 (|hi| < 2^43, |lo| < 2^51), then one rounding
           const double hi = fma(__int2double_rn((int)v[0][r]), 65536.0,
@@ -319,21 +391,23 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
           }
         }
       }
-      mbar_arrive(&sempty[buf]);
+      if (warp == EPI0 && lane == 0) I8_TRACE(it, 6);
+      i8_arrive(&sempty[buf]);
     }
   } else if (warp == MMAW) {
     // ---- MMA issuer ---------------------------------------------------------------
-    asm volatile("bar.sync 1, 288;\n" ::: "memory");
+    asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (I8_EPI_WARPS + 1)) : "memory");
     tc_fence_after();
     const uint32_t xbase = smem_u32(xdig);
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
-      mbar_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));
+      i8_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));
       tc_fence_after();
+      if (lane == 0) I8_TRACE(it, 3);
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
-        if (chunk_ctr >= 2) mbar_wait(&aempty[ab], (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
+        if (chunk_ctr >= 2) i8_wait(&aempty[ab], (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
         tc_fence_after();
         if (!(dbg & 1)) {
           const uint32_t dacc = tmem + (uint32_t)(I8_ACC0 + ab * I8_ACCBUF);
@@ -362,14 +436,17 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
         __syncwarp();
       }
       umma_commit_elect(&xempty[buf]);
+      if (lane == 0) I8_TRACE(it, 4);
       __syncwarp();
     }
   } else {
     // ---- slicer warps: rows 16w .. 16w+15 of each tile, from the smem stage ----
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
-      mbar_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));
-      if (it >= I8_NBUF) mbar_wait(&xempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
+      i8_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));
+      if (warp == 0 && lane == 0) I8_TRACE(it, 1);
+      if (it >= I8_NBUF) i8_wait(&xempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
+      if (warp == 0 && lane == 0) I8_TRACE(it, 7);
       unsigned char* planes = xdig + buf * I8_XBUF_BYTES;
       const double* xs = stage + buf * I8_TILE * I8_N;
       if (!(dbg & 2)) {
@@ -381,8 +458,9 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
 #pragma unroll
           for (int u = 0; u < RG; ++u) {
             const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
-            const double2 a0 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane);
-            const double2 a1 = *reinterpret_cast<const double2*>(xs + r * I8_N + 4 * lane + 2);
+            // k = 2l, 2l+1 and 64+2l, 65+2l (i8_kperm): two conflict-free 512 B rows
+            const double2 a0 = *reinterpret_cast<const double2*>(xs + r * I8_N + 2 * lane);
+            const double2 a1 = *reinterpret_cast<const double2*>(xs + r * I8_N + 64 + 2 * lane);
             xv[u][0] = a0.x; xv[u][1] = a0.y; xv[u][2] = a1.x; xv[u][3] = a1.y;
           }
 #pragma unroll
@@ -402,7 +480,16 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
             // what x T gives in fp64)
             const bool finite_row = bexp != 0x7ff;
             const int e = (m[u] == 0) ? 0 : bexp - 1022;  // max|x| < 2^e
-            const double scale = finite_row ? pow2(47 - e) : 0.0;
+            // 2^(47-e) and 2^(e-30) straight from the biased exponent (normal range);
+            // zero, tiny (bexp < 46) and non-finite rows take the general path
+            double scale, rs;
+            if (finite_row && bexp >= 46) {
+              scale = __longlong_as_double((long long)(2092 - bexp) << 52);
+              rs = __longlong_as_double((long long)(bexp - 29) << 52);
+            } else {
+              scale = finite_row ? pow2(47 - e) : 0.0;
+              rs = finite_row ? pow2(e - 30) : __longlong_as_double(0x7ff8000000000000ll);
+            }
             // round(x 2^(47-e)) as a 48-bit integer: the low word of fma(x, s, 1.5 2^52)
             // is the low word of the integer, the high word is offset by 0x43380000
             uint32_t vlo[4], vhi[4];
@@ -432,14 +519,14 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
             two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 1u, 0u, w[4], w[5]);  // bytes 1, 0
 #pragma unroll
             for (int p = 0; p < I8_ND; ++p) *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = w[p];
-            if (lane == 0)
-              rscale[buf * I8_TILE + r] = finite_row ? pow2(e - 30) : __longlong_as_double(0x7ff8000000000000ll);
+            if (lane == 0) rscale[buf * I8_TILE + r] = rs;
           }
         }
       }
       fence_proxy_async();
-      mbar_arrive(&xfull[buf]);
-      mbar_arrive(&sempty[buf]);
+      if (warp == 0 && lane == 0) I8_TRACE(it, 2);
+      i8_arrive(&xfull[buf]);
+      i8_arrive(&sempty[buf]);
     }
   }
   tc_fence_before();

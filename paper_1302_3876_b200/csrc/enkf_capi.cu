@@ -13,6 +13,7 @@
 #include "../../include/enkf_b200.h"
 #include "enkf_kernels.cuh"
 #include "anomaly_i8.cuh"
+#include "localized.cuh"
 
 using namespace enkf;
 
@@ -51,6 +52,10 @@ struct enkf_plan {
   bool ring_busy[2] = {false, false};  // an async DMA may still touch the slot
   int ring_next = 0;
   size_t ring_bytes = 0;
+  // localized-analysis workspace (lazily allocated): V, D, Z [n_obs][n]
+  double* locV = nullptr;
+  double* locD = nullptr;
+  double* locZ = nullptr;
 };
 
 namespace {
@@ -530,6 +535,9 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->hr);
   cudaFree(p->hidx);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  cudaFree(p->locV);
+  cudaFree(p->locD);
+  cudaFree(p->locZ);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
     if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
@@ -674,6 +682,80 @@ int32_t enkf_innovations_f64(const double* X, const double* Y, const int64_t* id
   const int64_t threads = n_obs * 32;
   innovations_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(X, Y, idx, D, n_obs, (int)n_ens);
   return cudaGetLastError() == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
+}
+
+namespace {
+// Shared body of the two localized entry points (enkf.py:187-199).
+int localized_common(enkf_plan* p, const double* X, const double* Y, const int64_t* idx, const double* r,
+                     const double* delta, double scale, int mode, double* XA, void* stream, enkf_status* st) {
+  if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (p->n < 2) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (mode == 1 && !(scale > 0.0)) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "influence scale must be positive");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  const int n = p->n;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t obs_elems = (size_t)p->n_obs * (size_t)n;
+  if (!p->locV && obs_elems) {
+    CUDA_TRY(cudaMalloc(&p->locV, sizeof(double) * obs_elems), st);
+    CUDA_TRY(cudaMalloc(&p->locD, sizeof(double) * obs_elems), st);
+    CUDA_TRY(cudaMalloc(&p->locZ, sizeof(double) * obs_elems), st);
+  }
+  const double root = std::sqrt((double)n - 1.0);
+  CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
+  if (p->n_obs > 0) {
+    const int64_t threads = p->n_obs * 32;
+    obs_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(X, Y, idx, p->locV, p->locD, p->n_obs,
+                                                                      p->n_state, n, root, p->dstatus);
+    CUDA_TRY(cudaGetLastError(), st);
+    CUDA_TRY(launch_gram(p, false, p->locV, p->locD, nullptr, r, p->gram, s), st);
+    CUDA_TRY(launch_levels(p, p->gram, p->A, nullptr, p->den, 0.0, s), st);
+    CUDA_TRY(launch_rowgemm<1>(p, p->locV, p->A, p->locD, r, p->locZ, p->n_obs, s), st);
+  }
+  if (p->n_state > 0) {
+    const size_t smem = localized_smem_bytes(n);
+    const unsigned grid = (unsigned)((p->n_state + LOC_TI - 1) / LOC_TI);
+    if (mode == 0) {
+      CUDA_TRY(cudaFuncSetAttribute(localized_update_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem), st);
+      localized_update_kernel<0><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, delta, idx, scale, XA,
+                                                                p->n_state, p->n_obs, n, root);
+    } else {
+      CUDA_TRY(cudaFuncSetAttribute(localized_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem), st);
+      localized_update_kernel<1><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, nullptr, idx, scale, XA,
+                                                                p->n_state, p->n_obs, n, root);
+    }
+    CUDA_TRY(cudaGetLastError(), st);
+  }
+  return enkf_plan_sync_status(p, stream, st);
+}
+}  // namespace
+
+int32_t enkf_analysis_localized_f64(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
+                                    const double* r, const double* delta, double* XA, void* stream,
+                                    enkf_status* st) {
+  if (p && p->n_state > 0 && p->n_obs > 0 && !delta) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "null influence matrix");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  return localized_common(p, X, Y, idx, r, delta, 0.0, 0, XA, stream, st);
+}
+
+int32_t enkf_analysis_localized_cyclic_f64(enkf_plan* p, const double* X, const double* Y,
+                                           const int64_t* idx, const double* r, double scale, double* XA,
+                                           void* stream, enkf_status* st) {
+  return localized_common(p, X, Y, idx, r, nullptr, scale, 1, XA, stream, st);
+}
+
+// Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
+// int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
+__attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, enkf::g_i8_trace, sizeof(enkf::g_i8_trace)) == cudaSuccess ? 0 : 5;
 }
 
 }  // extern "C"

@@ -187,14 +187,13 @@ def analysis_step(
     """One stochastic-EnKF analysis update, X^A = X + S (V'Z) (enkf.py:167-192).
 
     Same signature as the reference.  ``solver`` must be "sherman" (the other
-    reference solvers are not on this path); ``localization`` is not
-    supported (the dense Nstate x Nobs influence matrix is out of scope);
-    ``workers`` is accepted and ignored (the GPU result does not depend on it).
-    Returns a new array; inputs are never modified.
+    reference solvers are not on this path); ``workers`` is accepted and
+    ignored (the GPU result does not depend on it).  ``localization`` is the
+    (nstate, nobs) influence matrix of enkf.py:193-199: a dense array/tensor,
+    or the lazy ``influence_matrix_cyclic`` object, which is evaluated on the
+    fly (matrix-free).  Returns a new array; inputs are never modified.
     """
     _require_sherman(solver)
-    if localization is not None:
-        raise NotImplementedError("localized analysis (enkf.py:193-199) is not on the B200 path")
     dev_in = _is_cuda_tensor(x)
     if not dev_in:
         x = np.asarray(x, dtype=float)
@@ -214,6 +213,9 @@ def analysis_step(
         raise ValueError("observation variances must be positive")
     if not np.all(np.isfinite(r_host)):
         raise ValueError("inputs contain non-finite entries")
+
+    if localization is not None:
+        return _analysis_localized(x, perturbed, h, r, localization, nstate, nobs, nens, dev_in)
 
     if dev_in:
         device = x.device
@@ -248,3 +250,97 @@ def analysis_step(
             ctypes.byref(st))
     _native.raise_for_status(code, st, "enkf_analysis_host_f64")
     return out
+
+
+class CyclicInfluence:
+    """Lazy ``influence_matrix_cyclic`` (enkf.py:138-164).
+
+    Entry (i, j) is exp(-d(i, p_j) / scale), d the cyclic index distance
+    min(|i - p|, nstate - |i - p|) and p_j the state index of observation j.
+    ``np.asarray(obj)`` materialises exactly the reference's dense matrix (and
+    indexing / ``min`` / ``max`` go through it), but ``analysis_step`` never
+    does: it evaluates the taper inside the localized-update kernel, so the
+    Nstate x Nobs matrix is not formed at any size.
+    """
+
+    ndim = 2
+    dtype = np.dtype(np.float64)
+
+    def __init__(self, nstate: int, h: SelectionOperator, scale: float):
+        self.nstate = int(nstate)
+        self.h = h
+        self.scale = float(scale)
+        self.shape = (self.nstate, h.nobs(self.nstate))
+
+    def _obs_idx(self):
+        return np.arange(self.nstate) if self.h.indices is None else self.h.indices
+
+    def __array__(self, dtype=None, copy=None):
+        i = np.arange(self.nstate)[:, None]
+        raw = np.abs(i - self._obs_idx()[None, :])
+        dist = np.minimum(raw, self.nstate - raw)
+        out = np.exp(-dist / self.scale)
+        return out if dtype is None else out.astype(dtype)
+
+    def __getitem__(self, key):
+        return np.asarray(self)[key]
+
+    def min(self):
+        return np.asarray(self).min()
+
+    def max(self):
+        return np.asarray(self).max()
+
+    def same_operator(self, h: SelectionOperator) -> bool:
+        if self.h.indices is None or h.indices is None:
+            return self.h.indices is None and h.indices is None
+        return self.h.indices.shape == h.indices.shape and bool(np.array_equal(self.h.indices, h.indices))
+
+
+def influence_matrix_cyclic(nstate: int, h: SelectionOperator, scale: float | None = None) -> CyclicInfluence:
+    """Distance-based impact factors for a periodic 1-D state (enkf.py:138-164):
+    same arguments, defaults and ValueErrors as the reference; returns the lazy
+    :class:`CyclicInfluence` (array-convertible to the reference's matrix)."""
+    if scale is None:
+        scale = float(nstate)
+    if scale <= 0:
+        raise ValueError("influence scale must be positive")
+    if h.indices is not None and h.indices[-1] >= nstate:
+        raise ValueError("observation index out of range")
+    return CyclicInfluence(nstate, h, scale)
+
+
+def _analysis_localized(x, perturbed, h, r, localization, nstate, nobs, nens, dev_in):
+    """enkf.py:193-199: X + (Delta o (S V')) Z on the GPU (localized_update_kernel)."""
+    cyclic = isinstance(localization, CyclicInfluence) and localization.same_operator(h) \
+        and localization.nstate == nstate
+    if cyclic:
+        shape = localization.shape
+    elif _is_cuda_tensor(localization):
+        shape = tuple(localization.shape)
+    else:
+        localization = np.asarray(localization, dtype=float)
+        shape = localization.shape
+    if tuple(shape) != (nstate, nobs):
+        raise ValueError(f"influence matrix shape {tuple(shape)} does not match "
+                         f"(nstate, nobs) = ({nstate}, {nobs})")
+    device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
+    plan = _native.get_plan(device.index, nstate, nobs, nens)
+    xd = _f64_contig_device(x, device)
+    yd = _f64_contig_device(perturbed, device)
+    rd = _f64_contig_device(r, device)
+    idx = h.device_indices(device)
+    out = torch.empty_like(xd)
+    st = _native.EnkfStatus()
+    with plan.lock:
+        if cyclic:
+            code = _native.lib().enkf_analysis_localized_cyclic_f64(
+                plan.handle, xd.data_ptr(), yd.data_ptr(), 0 if idx is None else idx.data_ptr(),
+                rd.data_ptr(), localization.scale, out.data_ptr(), _stream_ptr(device), ctypes.byref(st))
+        else:
+            dd = _f64_contig_device(localization, device)
+            code = _native.lib().enkf_analysis_localized_f64(
+                plan.handle, xd.data_ptr(), yd.data_ptr(), 0 if idx is None else idx.data_ptr(),
+                rd.data_ptr(), dd.data_ptr(), out.data_ptr(), _stream_ptr(device), ctypes.byref(st))
+    _native.raise_for_status(code, st, "enkf_analysis_localized_f64")
+    return out if dev_in else out.cpu().numpy()

@@ -1,7 +1,7 @@
 """Generate the golden fixtures by running the REFERENCE itself.
 
 Run in the build container (the reference is importable only there):
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [fixture ...]
 It imports `enkfkit` from /root/reference/pkg/src (read-only) and writes
 small .npz files next to this script.  The GPU box never reads the reference;
 tests compare the oracle restatement (CPU tests) and the CUDA path (GPU tests)
@@ -152,9 +152,59 @@ def selections():
     return out
 
 
+def localized():
+    """Localized analysis (enkf.py:193-199) with the reference's own
+    influence_matrix_cyclic (enkf.py:138-164): the lorenz-small preset shape
+    (40 x 20, fully observed, scale 8), a partially observed ring, a random
+    dense influence matrix (test_enkf.py:235-252 style) and unit influence
+    (test_enkf.py:254-260)."""
+    out = {}
+    rng = make_rng(0xA5)
+    cases = [(40, 20, None, 8.0, "cyclic"), (64, 12, 16, 5.0, "cyclic"), (9, 4, 5, None, "uniform"),
+             (10, 4, 6, None, "ones"), (130, 33, 40, None, "cyclic"), (50, 7, 50, 3.0, "cyclic")]
+    for i, (nstate, nens, nobs, scale, kind) in enumerate(cases):
+        x = rng.standard_normal((nstate, nens)) + 8.0
+        if nobs is None:
+            h = ref_enkf.SelectionOperator.identity()
+            m = nstate
+        else:
+            idx = np.sort(rng.choice(nstate, size=nobs, replace=False))
+            h = ref_enkf.SelectionOperator.from_indices(idx)
+            m = nobs
+        r = rng.uniform(0.2, 1.0, m)
+        y = rng.standard_normal(m) + 8.0
+        eps = 0.5 * rng.standard_normal((m, nens))
+        obs = ref_enkf.ObservationBatch(y=y, perturbed=y[:, None] + eps, perturbations=eps)
+        if kind == "cyclic":
+            delta = ref_enkf.influence_matrix_cyclic(nstate, h, scale=scale)
+        elif kind == "uniform":
+            delta = rng.uniform(0.0, 1.0, (nstate, m))
+        else:
+            delta = np.ones((nstate, m))
+        xa = ref_enkf.analysis_step(x, obs, h, r, "sherman", localization=delta)
+        out[f"l{i}_x"] = x
+        out[f"l{i}_idx"] = np.array([]) if h.indices is None else h.indices
+        out[f"l{i}_identity"] = np.array(h.indices is None)
+        out[f"l{i}_r"] = r
+        out[f"l{i}_perturbed"] = obs.perturbed
+        out[f"l{i}_delta"] = delta
+        out[f"l{i}_kind"] = np.array(kind)
+        out[f"l{i}_scale"] = np.array(np.nan if scale is None else scale)
+        out[f"l{i}_xa"] = xa
+    out["ncases"] = np.array(len(cases))
+    # influence_matrix_cyclic known answers (test_enkf.py:160-190)
+    for tag, (ns, idx, sc) in {"i0": (10, [0, 5], None), "i1": (10, [5], None), "i2": (10, [9], None),
+                               "i3": (17, None, None), "i4": (10, [5], 2.0), "i5": (40, None, 8.0)}.items():
+        h = ref_enkf.SelectionOperator.identity() if idx is None else ref_enkf.SelectionOperator.from_indices(idx)
+        out[f"{tag}_delta"] = ref_enkf.influence_matrix_cyclic(ns, h, scale=sc)
+    return out
+
+
 if __name__ == "__main__":
-    for name, fn in (("ism_systems", ism_systems), ("analysis_small", analysis_small),
+    for name, fn in (("localized", localized), ("ism_systems", ism_systems), ("analysis_small", analysis_small),
                      ("configs", config_fixtures), ("selection", selections)):
+        if len(sys.argv) > 1 and name not in sys.argv[1:]:
+            continue  # e.g. `make_golden.py localized` regenerates one fixture
         data = fn()
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **data)

@@ -44,3 +44,15 @@ def rel_err(a, b):
     """Normwise max convention of the reference tests: max|a-b| / max|b|."""
     a, b = np.asarray(a), np.asarray(b)
     return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def localized_cases():
+    """Yield dicts with x, idx (None = identity), r, perturbed, delta, kind, scale, xa."""
+    g = load("localized")
+    for i in range(int(g["ncases"])):
+        c = {k: g[f"l{i}_{k}"] for k in ("x", "r", "perturbed", "delta", "xa")}
+        c["idx"] = None if bool(g[f"l{i}_identity"]) else g[f"l{i}_idx"].astype(np.int64)
+        c["kind"] = str(g[f"l{i}_kind"])
+        sc = float(g[f"l{i}_scale"])
+        c["scale"] = None if np.isnan(sc) else sc
+        yield c

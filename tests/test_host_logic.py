@@ -80,8 +80,11 @@ def test_analysis_step_argument_errors_before_device():
         P.analysis_step(np.ones((6, 4)), obs, h, np.array([1.0, -1.0]))
     with pytest.raises(ValueError):
         P.analysis_step(np.ones((6, 4)), obs, h, np.ones(3))
-    with pytest.raises(NotImplementedError):
-        P.analysis_step(np.ones((6, 4)), obs, h, np.ones(2), localization=np.ones((6, 2)))
+    with pytest.raises(ValueError):  # influence matrix shape (enkf.py:194-198), checked before the device
+        P.analysis_step(np.ones((6, 4)), obs, h, np.ones(2), localization=np.ones((3, 3)))
+    with pytest.raises(ValueError):
+        P.analysis_step(np.ones((6, 4)), obs, h, np.ones(2),
+                        localization=P.influence_matrix_cyclic(7, P.SelectionOperator.identity()))
     with pytest.raises(ValueError):
         P.analysis_step(np.ones((6, 4)), obs, h, np.ones(2), solver="nope")
 
