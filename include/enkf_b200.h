@@ -20,6 +20,8 @@
  *   enkf_analysis_localized_f64        enkf.py:193-199  analysis_step(..., localization=delta)
  *   enkf_analysis_localized_cyclic_f64 enkf.py:193-199 with delta = influence_matrix_cyclic
  *                           (enkf.py:138-164) evaluated on the fly (matrix-free)
+ *   enkf_forecast_l96_f64   models/lorenz96.py:31-78  Lorenz96.advance (RK4 steps), bit-exact
+ *   enkf_cycle_l96_f64      experiment.py:457-479     forecast -> analysis cycles, device-resident
  *
  * Layouts (all fp64 row-major, the reference's C-order arrays):
  *   X, XA : [n_state][n_ens]      Y, D, V, Z : [n_obs][n_ens]
@@ -35,6 +37,8 @@
  *   ENKF_SINGULAR_UPDATE    -> SingularUpdateError(level, denominator) (sherman.py:171-174)
  *   ENKF_NOT_SUPPORTED      -> NotImplementedError (shape outside the kernels' range)
  *   ENKF_CUDA_ERROR         -> RuntimeError
+ *   ENKF_DIVERGED           -> DivergenceError(member) (models/lorenz96.py:52-58; status.level
+ *                              = the first non-finite ensemble column)
  */
 #ifndef ENKF_B200_H
 #define ENKF_B200_H
@@ -51,7 +55,8 @@ enum enkf_code {
   ENKF_INDEX_RANGE = 2,
   ENKF_SINGULAR_UPDATE = 3,
   ENKF_NOT_SUPPORTED = 4,
-  ENKF_CUDA_ERROR = 5
+  ENKF_CUDA_ERROR = 5,
+  ENKF_DIVERGED = 6
 };
 
 typedef struct enkf_status {
@@ -116,6 +121,25 @@ int32_t enkf_analysis_localized_f64(enkf_plan* plan, const double* X, const doub
 int32_t enkf_analysis_localized_cyclic_f64(enkf_plan* plan, const double* X, const double* Y,
                                            const int64_t* idx, const double* r, double scale,
                                            double* XA, void* stream, enkf_status* status);
+
+/* Lorenz-96 ensemble forecast (models/lorenz96.py:31-78, enkf.py:202-212):
+ * n_steps RK4 steps of size dt with forcing F on the plan's [n_state][n_ens]
+ * ensemble, every member independently; X and Xout may alias.  Same
+ * operation order as the reference (no FMA contraction): bit-identical.
+ * A non-finite state returns ENKF_DIVERGED with status.level = first bad member. */
+int32_t enkf_forecast_l96_f64(enkf_plan* plan, const double* X, double* Xout, double dt, double forcing,
+                              int32_t n_steps, void* stream, enkf_status* status);
+/* Device-resident cycled assimilation (the experiment.py:457-479 loop with the
+ * lorenz96 model and pre-staged perturbed observations):
+ *   for c in [0, n_cycles): X <- forecast(X, steps_per_cycle); X <- analysis(X, Ys[c], idx, r)
+ * X is updated in place.  Ys: [n_cycles][n_obs][n_ens].  mean_f / mean_a
+ * (optional, [n_cycles][n_state]) receive the forecast / analysis ensemble
+ * means.  No host round trip between cycles; the first failing cycle (0-based)
+ * is returned in *failed_cycle (-1 if none) with its error in status. */
+int32_t enkf_cycle_l96_f64(enkf_plan* plan, double* X, const double* Ys, const int64_t* idx, const double* r,
+                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing,
+                           double* mean_f, double* mean_a, void* stream, enkf_status* status,
+                           int32_t* failed_cycle);
 
 /* --- staged form (multi-GPU: partial Gram -> allreduce by the caller -> levels) --- */
 

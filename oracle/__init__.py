@@ -16,13 +16,18 @@ running the reference itself in the build container
 from .enkf_oracle import (  # noqa: F401
     GROUP_LEVELS,
     SINGULAR_TOL,
+    OracleDivergence,
     OracleSingularUpdate,
     analysis_step,
     analysis_step_chunked,
     analysis_step_localized,
     apply_selection,
+    cycle_l96,
     influence_matrix_cyclic,
     innovations,
+    l96_advance,
+    l96_rk4_step,
+    l96_tendency,
     long_op_count,
     member_deviations,
     solve_sherman,

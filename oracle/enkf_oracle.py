@@ -223,3 +223,52 @@ def analysis_step_localized(x, perturbed, indices, r, delta):
         raise ValueError(f"influence matrix shape {delta.shape} does not match "
                          f"(nstate, nobs) = ({x.shape[0]}, {v.shape[0]})")
     return x + (delta * (s @ v.T)) @ z
+
+
+class OracleDivergence(ArithmeticError):
+    """models/lorenz96.py:52-58: the state became non-finite; ``member`` is the
+    first non-finite ensemble column."""
+
+    def __init__(self, member):
+        self.member = member
+        super().__init__(f"state became non-finite (ensemble member {member})")
+
+
+def l96_tendency(x, forcing):
+    """models/lorenz96.py:31-39 (cyclic in the first axis)."""
+    return (np.roll(x, -1, axis=0) - np.roll(x, 2, axis=0)) * np.roll(x, 1, axis=0) - x + forcing
+
+
+def l96_rk4_step(x, dt, forcing):
+    """models/lorenz96.py:42-49."""
+    k1 = l96_tendency(x, forcing)
+    k2 = l96_tendency(x + 0.5 * dt * k1, forcing)
+    k3 = l96_tendency(x + 0.5 * dt * k2, forcing)
+    k4 = l96_tendency(x + dt * k3, forcing)
+    return x + (dt / 6.0) * (k1 + 2.0 * k2 + 2.0 * k3 + k4)
+
+
+def l96_advance(x, nsteps, dt=0.05, forcing=8.0):
+    """models/lorenz96.py:52-78: nsteps RK4 steps, finiteness checked after each."""
+    x = np.asarray(x, dtype=float)
+    for _ in range(nsteps):
+        x = l96_rk4_step(x, dt, forcing)
+        if not np.all(np.isfinite(x)):
+            if x.ndim == 2:
+                raise OracleDivergence(int(np.argmax(~np.isfinite(x).all(axis=0))))
+            raise OracleDivergence(None)
+    return x
+
+
+def cycle_l96(x0, ys, indices, r, steps_per_cycle, dt=0.05, forcing=8.0):
+    """experiment.py:457-479 closed loop with the lorenz96 model: forecast
+    (enkf.py:202-212) then analysis_step, per cycle; returns the final
+    ensemble and the forecast / analysis ensemble means per cycle."""
+    x = np.asarray(x0, dtype=float)
+    mean_f, mean_a = [], []
+    for y in ys:
+        x = l96_advance(x, steps_per_cycle, dt, forcing)
+        mean_f.append(x.mean(axis=1))
+        x = analysis_step(x, y, indices, r)
+        mean_a.append(x.mean(axis=1))
+    return x, np.stack(mean_f), np.stack(mean_a)

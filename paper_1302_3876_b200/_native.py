@@ -24,6 +24,7 @@ ENKF_INDEX_RANGE = 2
 ENKF_SINGULAR_UPDATE = 3
 ENKF_NOT_SUPPORTED = 4
 ENKF_CUDA_ERROR = 5
+ENKF_DIVERGED = 6
 
 
 class EnkfStatus(ctypes.Structure):
@@ -60,6 +61,9 @@ PROTOTYPES = {
     "enkf_innovations_f64": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
     "enkf_analysis_localized_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _st]),
     "enkf_analysis_localized_cyclic_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _st]),
+    "enkf_forecast_l96_f64": (_i32, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_double, _i32, _vp, _st]),
+    "enkf_cycle_l96_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_double, ctypes.c_double,
+                                  _vp, _vp, _vp, _st, ctypes.POINTER(_i32)]),
 }
 
 _lib = None
@@ -114,6 +118,9 @@ def raise_for_status(code: int, status: EnkfStatus | None, what: str = "") -> No
         raise SingularUpdateError(int(status.level), float(status.denominator))
     if code == ENKF_NOT_SUPPORTED:
         raise NotImplementedError(msg)
+    if code == ENKF_DIVERGED:
+        from .errors import DivergenceError
+        raise DivergenceError("state became non-finite", member=int(status.level))
     raise RuntimeError(f"CUDA error in {what}: {msg}")
 
 

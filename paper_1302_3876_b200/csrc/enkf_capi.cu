@@ -14,6 +14,7 @@
 #include "enkf_kernels.cuh"
 #include "anomaly_i8.cuh"
 #include "localized.cuh"
+#include "l96.cuh"
 
 using namespace enkf;
 
@@ -56,6 +57,10 @@ struct enkf_plan {
   double* locV = nullptr;
   double* locD = nullptr;
   double* locZ = nullptr;
+  // Lorenz-96 forecast workspace for rings too long for shared memory: 3 x [n_state][n]
+  double* l96ws = nullptr;
+  DevStatus* cyc_status = nullptr;  // per-cycle status of enkf_cycle_l96_f64
+  int cyc_cap = 0;
 };
 
 namespace {
@@ -359,6 +364,14 @@ cudaError_t copy_d2h(enkf_plan* p, void* dst, const void* src, size_t bytes, cud
 
 int translate_status(const enkf_plan* p, enkf_status* st) {
   const DevStatus& d = *p->hstatus;
+  if (d.flags & FLAG_DIVERGED) {  // the forecast precedes the analysis of its cycle
+    const unsigned long long key = ~(unsigned long long)d.bad_index;
+    const int member = (int)(key & 0xffffffffu);
+    set_status(st, ENKF_DIVERGED, "state became non-finite (ensemble member %d, step %d)", member,
+               (int)(key >> 32));
+    if (st) st->level = member;
+    return ENKF_DIVERGED;
+  }
   if (d.flags & (FLAG_IDX_RANGE)) {
     set_status(st, ENKF_INDEX_RANGE, "observation index out of range for state size %lld",
                (long long)p->n_state);
@@ -538,6 +551,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->locV);
   cudaFree(p->locD);
   cudaFree(p->locZ);
+  cudaFree(p->l96ws);
+  cudaFree(p->cyc_status);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
     if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
@@ -750,6 +765,140 @@ int32_t enkf_analysis_localized_cyclic_f64(enkf_plan* p, const double* X, const 
                                            const int64_t* idx, const double* r, double scale, double* XA,
                                            void* stream, enkf_status* st) {
   return localized_common(p, X, Y, idx, r, nullptr, scale, 1, XA, stream, st);
+}
+
+namespace {
+// n_steps RK4 steps of the plan's ensemble, X -> Xout (may alias), on stream s.
+cudaError_t launch_l96(enkf_plan* p, const double* X, double* Xout, double dt, double forcing, int n_steps,
+                       cudaStream_t s) {
+  const int64_t ns = p->n_state;
+  const int n = p->n;
+  const double half_dt = 0.5 * dt, dt6 = dt / 6.0;  // the reference's scalar factors
+  if (ns == 0 || n == 0) return cudaSuccess;
+  if (n_steps == 0) {
+    return X == Xout ? cudaSuccess
+                     : cudaMemcpyAsync(Xout, X, sizeof(double) * (size_t)ns * n, cudaMemcpyDeviceToDevice, s);
+  }
+  int mb = (int)std::min<int64_t>((int64_t)(L96_SMEM_MAX / (32 * (size_t)ns)), (int64_t)n);
+  if (mb >= 1) {
+    const size_t smem = 32 * (size_t)ns * mb;
+    cudaError_t e = cudaFuncSetAttribute(l96_rk4_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    l96_rk4_smem_kernel<<<(n + mb - 1) / mb, L96_THREADS, smem, s>>>(X, Xout, ns, n, mb, half_dt, dt, dt6,
+                                                                      forcing, n_steps, p->dstatus);
+    return cudaGetLastError();
+  }
+  if (!p->l96ws) {
+    cudaError_t e = cudaMalloc(&p->l96ws, 3 * sizeof(double) * (size_t)ns * n);
+    if (e != cudaSuccess) return e;
+  }
+  double* sa = p->l96ws;
+  double* sb = sa + (size_t)ns * n;
+  double* acc = sb + (size_t)ns * n;
+  if (X != Xout) {
+    cudaError_t e = cudaMemcpyAsync(Xout, X, sizeof(double) * (size_t)ns * n, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+  }
+  const int grid = std::max(1, std::min(p->num_sms * 8, (int)((ns * n + 255) / 256)));
+  for (int step = 0; step < n_steps; ++step) {
+    l96_stage_kernel<<<grid, 256, 0, s>>>(Xout, Xout, acc, sa, ns, n, 0, half_dt, dt, dt6, forcing, step, p->dstatus);
+    l96_stage_kernel<<<grid, 256, 0, s>>>(Xout, sa, acc, sb, ns, n, 1, half_dt, dt, dt6, forcing, step, p->dstatus);
+    l96_stage_kernel<<<grid, 256, 0, s>>>(Xout, sb, acc, sa, ns, n, 2, half_dt, dt, dt6, forcing, step, p->dstatus);
+    l96_stage_kernel<<<grid, 256, 0, s>>>(Xout, sa, acc, Xout, ns, n, 3, half_dt, dt, dt6, forcing, step, p->dstatus);
+  }
+  return cudaGetLastError();
+}
+
+int check_l96(const enkf_plan* p, double dt, int n_steps, enkf_status* st) {
+  if (p->n_state < 4) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "state must have at least 4 components");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (!(dt > 0.0)) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "dt must be positive");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (n_steps < 0) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "negative step count");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  return ENKF_OK;
+}
+}  // namespace
+
+int32_t enkf_forecast_l96_f64(enkf_plan* p, const double* X, double* Xout, double dt, double forcing,
+                              int32_t n_steps, void* stream, enkf_status* st) {
+  if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (int rc = check_l96(p, dt, n_steps, st)) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
+  CUDA_TRY(launch_l96(p, X, Xout, dt, forcing, n_steps, s), st);
+  return enkf_plan_sync_status(p, stream, st);
+}
+
+int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, const double* r,
+                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing,
+                           double* mean_f, double* mean_a, void* stream, enkf_status* st,
+                           int32_t* failed_cycle) {
+  if (failed_cycle) *failed_cycle = -1;
+  if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (p->n < 2) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (int rc = check_l96(p, dt, steps_per_cycle, st)) return rc;
+  if (n_cycles < 0) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "negative cycle count");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (n_cycles == 0) {
+    set_status(st, ENKF_OK, "ok");
+    return ENKF_OK;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->cyc_cap < n_cycles) {
+    cudaFree(p->cyc_status);
+    p->cyc_status = nullptr;
+    p->cyc_cap = 0;
+    CUDA_TRY(cudaMalloc(&p->cyc_status, sizeof(DevStatus) * (size_t)n_cycles), st);
+    p->cyc_cap = n_cycles;
+  }
+  CUDA_TRY(cudaMemsetAsync(p->cyc_status, 0, sizeof(DevStatus) * (size_t)n_cycles, s), st);
+  DevStatus* saved = p->dstatus;
+  const double cscale = 1.0 / std::sqrt((double)(p->n - 1));
+  const size_t yelems = (size_t)p->n_obs * p->n;
+  const unsigned mean_grid = (unsigned)((p->n_state * 32 + 255) / 256);
+  cudaError_t e = cudaSuccess;
+  for (int c = 0; c < n_cycles && e == cudaSuccess; ++c) {
+    p->dstatus = p->cyc_status + c;  // every kernel of cycle c flags into its own status
+    e = launch_l96(p, X, X, dt, forcing, steps_per_cycle, s);
+    if (e == cudaSuccess && mean_f) {
+      row_mean_kernel<<<mean_grid, 256, 0, s>>>(X, mean_f + (size_t)c * p->n_state, p->n_state, p->n);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = launch_gram(p, true, X, Ys + (size_t)c * yelems, idx, r, p->gram, s);
+    if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);
+    if (e == cudaSuccess) e = launch_rowgemm<0>(p, X, p->T, nullptr, nullptr, X, p->n_state, s);
+    if (e == cudaSuccess && mean_a) {
+      row_mean_kernel<<<mean_grid, 256, 0, s>>>(X, mean_a + (size_t)c * p->n_state, p->n_state, p->n);
+      e = cudaGetLastError();
+    }
+  }
+  p->dstatus = saved;
+  if (e != cudaSuccess) return cuda_fail(st, e, "enkf_cycle_l96_f64 launch");
+  std::vector<DevStatus> hs((size_t)n_cycles);
+  CUDA_TRY(cudaMemcpyAsync(hs.data(), p->cyc_status, sizeof(DevStatus) * (size_t)n_cycles, cudaMemcpyDeviceToHost,
+                           s), st);
+  CUDA_TRY(cudaStreamSynchronize(s), st);
+  for (int c = 0; c < n_cycles; ++c) {
+    if (hs[(size_t)c].flags == 0) continue;
+    *p->hstatus = hs[(size_t)c];
+    if (failed_cycle) *failed_cycle = c;
+    return translate_status(p, st);
+  }
+  set_status(st, ENKF_OK, "ok");
+  return ENKF_OK;
 }
 
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the

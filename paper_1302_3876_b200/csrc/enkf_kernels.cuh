@@ -40,6 +40,7 @@ enum : int {
   FLAG_IDX_ORDER = 4,
   FLAG_IDX_RANGE = 8,
   FLAG_SINGULAR = 16,
+  FLAG_DIVERGED = 32,  // Lorenz-96 forecast became non-finite (bad_index = ~(step << 32 | member))
 };
 
 constexpr double kSingularTol = 1e-14;  // sherman.py:51

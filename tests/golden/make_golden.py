@@ -200,8 +200,62 @@ def localized():
     return out
 
 
+def lorenz96():
+    """Lorenz96.advance (models/lorenz96.py:31-78) on seeded ensembles, the
+    DivergenceError member, and a short closed-loop cycle of forecast_step +
+    analysis_step (experiment.py:457-479) at a reduced config-2 shape."""
+    from enkfkit.enkf import forecast_step, perturb_observations
+    from enkfkit.errors import DivergenceError
+    out = {}
+    rng = make_rng(0xA7)
+    # inputs regenerated from the per-case seed (tests/golden_io.l96_input); outputs
+    # pinned bitwise by sha256 plus a strided row sample for diagnostics
+    cases = [(40, 20, 10), (4096, 8, 5), (7000, 3, 2), (4, 2, 3), (33, 1, 7), (1000, 64, 1)]
+    for i, (ns, nens, steps) in enumerate(cases):
+        x = 8.0 + make_rng(0xB000 + i).standard_normal((ns, nens))
+        model = Lorenz96(Lorenz96Config(nstate=ns, forcing=8.0, dt=0.05))
+        xf = model.advance(x, 0.0, steps * 0.05)
+        out[f"f{i}_meta"] = np.array([0xB000 + i, ns, nens, steps])
+        out[f"f{i}_xf_sha"] = np.array(sha(xf))
+        out[f"f{i}_xf_rows"] = xf[::max(1, ns // 64)]
+    out["nforecast"] = np.array(len(cases))
+    x1 = 8.0 + rng.standard_normal(40)
+    out["single_x"], out["single_xf"] = x1, Lorenz96(Lorenz96Config(nstate=40)).advance(x1, 0.0, 0.25)
+    # divergence: huge members overflow; the reference names the first bad column
+    xd = 8.0 + rng.standard_normal((16, 6))
+    xd[:, 4] *= 1e120
+    xd[:, 2] *= 1e160
+    try:
+        Lorenz96(Lorenz96Config(nstate=16)).advance(xd, 0.0, 0.5)
+        member = -1
+    except DivergenceError as exc:
+        member = exc.member
+    out["div_x"], out["div_member"] = xd, np.array(member)
+    # closed loop: ns=128, N=16, identity H, R = 0.1^2 I, 5 steps per cycle, 8 cycles
+    ns, nens, cycles = 128, 16, 8
+    model = Lorenz96(Lorenz96Config(nstate=ns))
+    truth = model.advance(8.0 + 0.01 * rng.standard_normal(ns), 0.0, 500 * 0.05)
+    x = truth[:, None] + rng.standard_normal((ns, nens))
+    r = np.full(ns, 0.01)
+    h = ref_enkf.SelectionOperator.identity()
+    out["cyc_x0"] = x
+    ys, mf, ma = [], [], []
+    for c in range(cycles):
+        truth = model.advance(truth, 0.0, 0.25)
+        y = truth + 0.1 * rng.standard_normal(ns)
+        ob = perturb_observations(y, r, nens, rng)
+        x = forecast_step(model, x, c * 0.25, (c + 1) * 0.25)
+        mf.append(x.mean(axis=1))
+        x = ref_enkf.analysis_step(x, ob, h, r, "sherman")
+        ma.append(x.mean(axis=1))
+        ys.append(ob.perturbed)
+    out["cyc_r"], out["cyc_ys"] = r, np.stack(ys)
+    out["cyc_mean_f"], out["cyc_mean_a"], out["cyc_xa"] = np.stack(mf), np.stack(ma), x
+    return out
+
+
 if __name__ == "__main__":
-    for name, fn in (("localized", localized), ("ism_systems", ism_systems), ("analysis_small", analysis_small),
+    for name, fn in (("lorenz96", lorenz96), ("localized", localized), ("ism_systems", ism_systems), ("analysis_small", analysis_small),
                      ("configs", config_fixtures), ("selection", selections)):
         if len(sys.argv) > 1 and name not in sys.argv[1:]:
             continue  # e.g. `make_golden.py localized` regenerates one fixture

@@ -56,3 +56,12 @@ def localized_cases():
         sc = float(g[f"l{i}_scale"])
         c["scale"] = None if np.isnan(sc) else sc
         yield c
+
+
+def l96_cases():
+    """Yield (ns, nens, steps, x, xf_sha, xf_rows, row_stride) of the Lorenz96.advance fixture."""
+    g = load("lorenz96")
+    for i in range(int(g["nforecast"])):
+        seed, ns, nens, steps = (int(t) for t in g[f"f{i}_meta"])
+        x = 8.0 + make_rng(seed).standard_normal((ns, nens))
+        yield ns, nens, steps, x, str(g[f"f{i}_xf_sha"]), g[f"f{i}_xf_rows"], max(1, ns // 64)
