@@ -74,12 +74,42 @@ def time_oracle(p, reps):
     return best, xa
 
 
+def time_cycled(cycles=100, cpu_cycles=5):
+    """Config 2 as the reference runs it: closed-loop cycles of 5 RK4 steps +
+    one analysis, device-resident (cycle_l96) vs the CPU oracle loop."""
+    cyc = W.Config2Cycler()
+    ns, nens = cyc.ns, cyc.nens
+    rng = np.random.Generator(np.random.Philox(0xC2))
+    ys = cyc.x.mean(axis=1)[None, :, None] + 0.1 * rng.standard_normal((cycles, ns, nens))
+    r = np.full(ns, 0.01)
+    model = P.Lorenz96(P.Lorenz96Config(nstate=ns))
+    h = P.SelectionOperator.identity()
+    dev = torch.device("cuda", 0)
+    x0 = torch.from_numpy(cyc.x).to(dev)
+    yd = torch.from_numpy(ys).to(dev)
+    P.cycle_l96(model, x0, yd[:3], h, r, 5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    P.cycle_l96(model, x0, yd, h, r, 5)
+    torch.cuda.synchronize()
+    gpu_s = (time.perf_counter() - t0) / cycles
+    t0 = time.perf_counter()
+    oracle.cycle_l96(cyc.x, ys[:cpu_cycles], None, r, 5)
+    cpu_s = (time.perf_counter() - t0) / cpu_cycles
+    return {"config2_cycled": {"cycles": cycles, "gpu_cycles_per_s": 1.0 / gpu_s, "gpu_ms_per_cycle": gpu_s * 1e3,
+                               "cpu_oracle_cycles_per_s": 1.0 / cpu_s, "cpu_sample_cycles": cpu_cycles,
+                               "cpu_threads": os.cpu_count(), "note": "wall clock incl. one sync per 100 cycles"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--cycled", action="store_true", help="also time the config-2 closed loop")
     a = ap.parse_args()
     out = {}
+    if a.cycled:
+        print(json.dumps(time_cycled()), flush=True)
     for cfg in [int(c) for c in a.configs.split(",")]:
         p = problem(cfg)
         reps = a.reps if cfg < 4 else 3
