@@ -70,6 +70,12 @@ __device__ __forceinline__ double i32_to_f64(uint32_t a) {
 // contiguous 512-byte LDS.128 rows (no bank conflicts).
 __host__ __device__ __forceinline__ int i8_kperm(int w, int b) { return (b < 2 ? 2 * w + b : 64 + 2 * w + b - 2); }
 
+#ifndef I8_EPI_MODE
+#define I8_EPI_MODE 0
+#endif
+#ifndef I8_CVT_MAGIC
+#define I8_CVT_MAGIC 0
+#endif
 #ifndef I8_WAIT_HINT
 #define I8_WAIT_HINT 1
 #endif
@@ -102,6 +108,17 @@ __device__ __forceinline__ void i8_arrive(uint64_t* bar) {
 #endif
 }
 constexpr int I8_ARRIVE_UNIT = I8_WARP_ARRIVE ? 1 : 32;
+
+// d 2^k for rows whose exponent shift leaves the exponent-field fast path
+// (|x| near the fp64 range limits): exact scaling, or NaN for non-finite rows.
+__device__ __noinline__ double i8_scale_slow(double d, int k) {
+  if (k == INT_MIN) return __longlong_as_double(0x7ff8000000000000ll);
+  if (d == 0.0) return 0.0;
+  if (k > 2000) return d * INFINITY;
+  if (k < -2200) return d * 0.0;
+  const int k1 = k / 2;
+  return d * ldexp(1.0, k1) * ldexp(1.0, k - k1);
+}
 
 // ---- tcgen05 helpers ---------------------------------------------------------
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
@@ -224,7 +241,7 @@ __device__ __forceinline__ uint32_t byte_of(long long v, int b) { return (uint32
 // 0 TMA issued, 1 stage landed (slicer view), 2 slicing done, 3 MMA issue start,
 // 4 MMA issue end, 5 epilogue first chunk ready, 6 epilogue done.
 constexpr int I8_TRACE_TILES = 256;
-__device__ unsigned long long g_i8_trace[I8_TRACE_TILES][8];
+__device__ unsigned long long g_i8_trace[I8_TRACE_TILES][16];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -234,8 +251,8 @@ __device__ __forceinline__ unsigned long long gtime() {
   do { if ((dbg & 8) && blockIdx.x == 0 && (it) < I8_TRACE_TILES) g_i8_trace[(it)][(ev)] = gtime(); } while (0)
 
 __global__ void __launch_bounds__(I8_THREADS, 1)
-anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* = T */,
-                  double* __restrict__ XA, int64_t n_rows, int dbg) {
+anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
+                  double* __restrict__ XA, int64_t n_rows, int dbg, uint32_t uz /* = 0 */) {
   // dbg (profiling only): bit0 skip MMAs, bit1 skip slicing, bit2 skip epilogue math/IO
   extern __shared__ __align__(1024) unsigned char i8sm_raw[];
   // realign by a byte offset (not an integer round trip) so the compiler keeps
@@ -243,16 +260,23 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   unsigned char* i8sm = i8sm_raw + ((1024u - (smem_u32(i8sm_raw) & 1023u)) & 1023u);
   unsigned char* xdig = i8sm;                                                  // [NBUF][6][32][128 B]
   double* stage = reinterpret_cast<double*>(xdig + I8_NBUF * I8_XBUF_BYTES);  // [NBUF][32][128]
-  // per-row scale factor [NBUF][32] = 2^(e-30) (NaN for non-finite rows)
-  double* rscale = stage + I8_NBUF * I8_TILE * I8_N;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rscale + I8_NBUF * I8_TILE);
+  // per-row exponent shift k [2*NBUF][32] (X^A = S' 2^k; INT_MIN for non-finite rows),
+  // a ring twice the stage depth so the slicers never overwrite a tile the epilogue reads
+  int* rinfo = reinterpret_cast<int*>(stage + I8_NBUF * I8_TILE * I8_N);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rinfo + 2 * I8_NBUF * I8_TILE);
   uint64_t* sfull = bars;                  // [NBUF] TMA -> slicers/epilogue      (count 1 + tx)
-  uint64_t* sempty = bars + I8_NBUF;       // [NBUF] slicers+epilogue -> producer (count slicer+epi)
+  uint64_t* sempty = bars + I8_NBUF;       // [NBUF] slicers -> producer              (count slicer warps)
   uint64_t* xfull = bars + 2 * I8_NBUF;    // [NBUF] slicers -> MMA               (count slicer threads)
   uint64_t* xempty = bars + 3 * I8_NBUF;   // [NBUF] MMA commit -> slicers        (count 1)
   uint64_t* afull = bars + 4 * I8_NBUF;    // [2] MMA commit -> epilogue          (count 1)
   uint64_t* aempty = bars + 4 * I8_NBUF + 2;  // [2] epilogue -> MMA              (count epi threads)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 4 * I8_NBUF + 4);
+  unsigned long long* cmax_s = reinterpret_cast<unsigned long long*>(bars + 4 * I8_NBUF + 5);  // max |T| bits
+  int* nonid_s = reinterpret_cast<int*>(bars + 4 * I8_NBUF + 6);  // T != I
+  // [2*NBUF] slicers -> epilogue: row exponents of a tile are in rinfo (count slicer
+  // threads).  Its own ring (depth 8 > the at most 5 tiles the slicers run ahead of
+  // the epilogue) keeps the parity waits unambiguous.
+  uint64_t* rfull = bars + 4 * I8_NBUF + 8;
 
   constexpr int EPI0 = I8_SLICE_WARPS;                 // first epilogue warp
   constexpr int MMAW = I8_SLICE_WARPS + I8_EPI_WARPS;  // MMA warp
@@ -264,15 +288,34 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   if (tid == 0) {
     for (int i = 0; i < I8_NBUF; ++i) {
       mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], I8_ARRIVE_UNIT * (I8_SLICE_WARPS + I8_EPI_WARPS));
+      mbar_init(&sempty[i], I8_ARRIVE_UNIT * I8_SLICE_WARPS);
       mbar_init(&xfull[i], I8_ARRIVE_UNIT * I8_SLICE_WARPS);
       mbar_init(&xempty[i], 1);
     }
+    for (int i = 0; i < 2 * I8_NBUF; ++i) mbar_init(&rfull[i], I8_ARRIVE_UNIT * I8_SLICE_WARPS);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&afull[i], 1);
       mbar_init(&aempty[i], I8_ARRIVE_UNIT * I8_EPI_WARPS);
     }
     fence_mbar_init();
+    *cmax_s = 0ull;
+    *nonid_s = 0;
+  }
+  __syncthreads();
+  {
+    // One power-of-two scale 2^fT for all of T (max|T| < 2^fT): the epilogue's
+    // per-output work then needs a per-row exponent only.  T == I exactly (zero
+    // spread) is detected so X^A = X comes out bit-exact.
+    unsigned long long lm = 0ull;
+    int nonid = 0;
+    for (int e = tid; e < I8_N * I8_N; e += I8_THREADS) {
+      const double tv = T[e];
+      const unsigned long long b = (unsigned long long)__double_as_longlong(tv) & 0x7fffffffffffffffull;
+      lm = b > lm ? b : lm;
+      nonid |= tv != ((e >> 7) == (e & 127) ? 1.0 : 0.0);
+    }
+    atomicMax(cmax_s, lm);
+    if (nonid) atomicOr(nonid_s, 1);
   }
   if (warp == MMAW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
@@ -287,8 +330,18 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
   // column 0: a compile-time TMEM base keeps every MMA operand uniform.
   constexpr uint32_t tmem = 0;
   if (tid == 0 && *tmem_slot != 0u) __trap();
-
-  if (warp == TMAW) {
+  const int fT = exp_above(*cmax_s);  // max|T| < 2^fT
+  if (*nonid_s == 0) {
+    // T == I: X^A = X exactly (the reference's zero-spread identity, test_enkf.py:208-213)
+    const int64_t ntiles_all = (n_rows + I8_TILE - 1) / I8_TILE;
+    for (int64_t tile = blockIdx.x; tile < ntiles_all; tile += gridDim.x) {
+      const int64_t g0 = tile * I8_TILE;
+      const int64_t rows = n_rows - g0 < I8_TILE ? n_rows - g0 : I8_TILE;
+      const double2* src = reinterpret_cast<const double2*>(X + g0 * I8_N);
+      double2* dst = reinterpret_cast<double2*>(XA + g0 * I8_N);
+      for (int64_t e = tid; e < rows * (I8_N / 2); e += I8_THREADS) dst[e] = src[e];
+    }
+  } else if (warp == TMAW) {
     // ---- producer: one bulk copy per tile (the tile's rows are contiguous) -----
     if (lane == 0) {
       for (int64_t it = 0; it < my_tiles; ++it) {
@@ -315,18 +368,11 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
     const int half = (warp - EPI0) >> 2;  // which I8_RPT rows of each 16-row chunk
     const int j = 32 * quad + lane;
-    // C^T digit planes into TMEM (A operand), column scale f_j
-    // C = T - I (T = I + (I - 11'/N) A / sqrt(N-1) from the levels kernel)
-    auto cval = [&](int k) { return C[k * I8_N + j] - (k == j ? 1.0 : 0.0); };
-    uint64_t cmax = 0;
-    for (int k = 0; k < I8_N; ++k) {
-      const uint64_t b = (uint64_t)__double_as_longlong(cval(k)) & 0x7fffffffffffffffull;
-      cmax = b > cmax ? b : cmax;
-    }
-    const int fj = exp_above(cmax);
-    const double fcol = pow2(fj);  // 2^f_j
+    // T^T digit planes into TMEM (A operand), one scale 2^(47-fT) for all of T
+    // (T = I + (I - 11'/N) A / sqrt(N-1) from the levels kernel)
+    auto cval = [&](int k) { return T[k * I8_N + j]; };
     if (half == 0) {
-      const double cscale = pow2(47 - fj);
+      const double cscale = pow2(47 - fT);
 #pragma unroll 1
       for (int p = 0; p < I8_ND; ++p) {
 #pragma unroll 1
@@ -348,9 +394,8 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
       const int64_t tile = blockIdx.x + it * gridDim.x;
-      i8_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // raw X of the tile is in smem
-      i8_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));  // and the slicers' row exponents
-      const double* xs = stage + buf * I8_TILE * I8_N;
+      i8_wait(&rfull[it % (2 * I8_NBUF)], (uint32_t)((it / (2 * I8_NBUF)) & 1));  // the tile's row exponents
+      const int* rk = rinfo + (int)(it % (2 * I8_NBUF)) * I8_TILE;
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
         const int r0 = c * I8_CHUNK + I8_RPT * half;  // first tile row of this thread's I8_RPT
@@ -358,6 +403,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
         i8_wait(&afull[ab], (uint32_t)((chunk_ctr >> 1) & 1));
         tc_fence_after();
         if (c == 0 && warp == EPI0 && lane == 0) I8_TRACE(it, 5);
+        if (warp == EPI0 && lane == 0) I8_TRACE(it, 12 + c);
         if (dbg & 4) {
           tc_fence_before();
           i8_arrive(&aempty[ab]);
@@ -371,28 +417,90 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
         tmem_ld_wait();
         tc_fence_before();
         i8_arrive(&aempty[ab]);  // accumulators copied out: the MMA may reuse them
-        const double* xrow = xs + r0 * I8_N + j;
-        const double* srow = rscale + buf * I8_TILE + r0;
-        double* orow = XA + g0 * I8_N + j;
-        const int nvalid = (int)(n_rows - g0 < I8_RPT ? n_rows - g0 : I8_RPT);
-#pragma unroll
-        for (int r = 0; r < I8_RPT; ++r) {
-          // X C = 2^(e+f-94) sum_l acc_l 256^(12-l): levels 2..4 -> hi, 5..8 -> lo,
-          // both exact in fp64 (|hi| < 2^43, |lo| < 2^51), then one rounding
-          const double hi = fma(__int2double_rn((int)v[0][r]), 65536.0,
-                                fma(__int2double_rn((int)v[1][r]), 256.0, __int2double_rn((int)v[2][r])));
-          const double lo = fma(__int2double_rn((int)v[3][r]), 16777216.0,
-                                fma(__int2double_rn((int)v[4][r]), 65536.0,
-                                    fma(__int2double_rn((int)v[5][r]), 256.0, __int2double_rn((int)v[6][r]))));
-          if (r < nvalid) {
-            const double sh = srow[r];  // 2^(e-30)
-            const double xc = fma(hi, sh, lo * (sh * 2.3283064365386963e-10)) * fcol;  // lo 2^(e-62)
-            orow[r * I8_N] = xrow[r * I8_N] + xc;
+        if (dbg & 16) {          // profiling: drain TMEM but skip the recombination and stores
+          // ... and burn 128 independent ops of one kind per thread (op = dbg >> 7):
+          // 1 DFMA, 2 IMAD, 3 IMAD.WIDE, 4 I2F.F64.S32, 5 DADD, 6 I2F.F64.S64, 7 DMUL
+          const int op = (dbg >> 7) & 31;
+          const int iters = (dbg >> 12) ? (dbg >> 12) : 32;  // x4 independent ops each
+          if (op == 1 || op == 5 || op == 7) {
+            double a0 = (double)v[0][0], a1 = (double)v[1][0], a2 = (double)v[2][0], a3 = (double)v[3][0];
+#pragma unroll 4
+            for (int i = 0; i < iters; ++i) {
+              if (op == 1) { a0 = fma(a0, 1.0000001, 0.5); a1 = fma(a1, 1.0000001, 0.5); a2 = fma(a2, 1.0000001, 0.5); a3 = fma(a3, 1.0000001, 0.5); }
+              if (op == 5) { a0 = a0 + 0.5; a1 = a1 + 0.5; a2 = a2 + 0.5; a3 = a3 + 0.5; }
+              if (op == 7) { a0 = a0 * 1.0000001; a1 = a1 * 1.0000001; a2 = a2 * 1.0000001; a3 = a3 * 1.0000001; }
+            }
+            if (a0 + a1 + a2 + a3 == 1234.5) XA[0] = 0.0;
+          } else if (op == 2 || op == 3) {
+            uint32_t a0 = v[0][0], a1 = v[1][0], a2 = v[2][0], a3 = v[3][0];
+            long long w0 = a0, w1 = a1, w2 = a2, w3 = a3;
+#pragma unroll 4
+            for (int i = 0; i < 32; ++i) {
+              if (op == 2) { a0 = a0 * 3u + 7u; a1 = a1 * 3u + 7u; a2 = a2 * 3u + 7u; a3 = a3 * 3u + 7u; }
+              if (op == 3) { w0 = (long long)(int)a0 * 65536 + w0; w1 = (long long)(int)a1 * 65536 + w1;
+                             w2 = (long long)(int)a2 * 65536 + w2; w3 = (long long)(int)a3 * 65536 + w3; }
+            }
+            if (a0 + a1 + a2 + a3 + (uint32_t)(w0 ^ w1 ^ w2 ^ w3) == 12345u) XA[0] = 0.0;
+          } else if (op == 4 || op == 6) {
+            unsigned long long acc = 0;
+#pragma unroll 8
+            for (int i = 0; i < 128; ++i) {
+              const uint32_t u = v[i & 7][0] + (uint32_t)i;
+              acc ^= (unsigned long long)__double_as_longlong((op == 4) ? __int2double_rn((int)u)
+                                                                        : (double)((long long)u << 20));
+            }
+            if (acc == 12345ull) XA[0] = 0.0;
           }
+          if (v[0][0] == 0x7fffffffu) XA[0] = 0.0;
+          continue;
         }
+        // profiling (dbg 32): stores cycle through a 1 MiB window (L2-resident, no DRAM writes)
+        double* orow = XA + ((dbg & 32) ? (g0 & 1023) : g0) * I8_N + j;
+        const int nvalid = (int)(n_rows - g0 < I8_RPT ? n_rows - g0 : I8_RPT);
+        // X T = 2^(e+fT-94) sum_l acc_l 256^(12-l).  On B200 FP64 arithmetic
+        // (DFMA/DMUL/DADD) shares hardware with the tensor cores: every FP64 op here
+        // stalls the concurrent int8 MMAs (measured, tools/probe/i8_trace.py; integer
+        // ops and int->fp64 conversions do not).  So the 7 levels are combined in
+        // INTEGER arithmetic into
+        //   S' = acc2 2^36 + acc3 2^28 + acc4 2^20 + acc5 2^12 + acc6 2^4 + (acc7 >> 4) + (acc8 >> 12)
+        // (|S'| < 2^63; S' is S / 2^12 up to 2 units, ~2^-57 of max|X||T|, far below
+        // the digit truncation), converted once (I2F.S64, one rounding) and scaled by
+        // 2^k, k = e + fT - 50, with an integer add to the exponent field.
+        int kr[I8_RPT];
+#pragma unroll
+        for (int r = 0; r < I8_RPT; r += 4) {
+          const int4 k4 = *reinterpret_cast<const int4*>(rk + r0 + r);
+          kr[r] = k4.x; kr[r + 1] = k4.y; kr[r + 2] = k4.z; kr[r + 3] = k4.w;
+        }
+        bool slow = false;  // rows near the fp64 range limits or non-finite (warp-uniform, rare)
+#pragma unroll
+        for (int r = 0; r < I8_RPT; ++r) slow |= (kr[r] < -1022) | (kr[r] > 961);
+        auto sprime = [&](int r) {
+          const int d2 = (int)v[0][r], d3 = (int)v[1][r], d4 = (int)v[2][r], d5 = (int)v[3][r];
+          const int d6 = (int)v[4][r], d7 = (int)v[5][r], d8 = (int)v[6][r];
+          const int small = d6 * 16 + ((d7 >> 4) + (d8 >> 12));  // |.| < 2^31
+          long long sp = (long long)d5 * 4096 + (long long)small;
+          sp += (long long)d4 * 1048576;
+          sp += (long long)d3 * 268435456;
+          sp += (long long)((unsigned long long)(unsigned)(d2 * 16) << 32);  // d2 2^36: high word only
+          return (double)sp;
+        };
+        if (!slow) {
+#pragma unroll
+          for (int r = 0; r < I8_RPT; ++r) {
+            const double dd = sprime(r);
+            const int hi = __double2hiint(dd);
+            const double res = __hiloint2double(hi == 0 ? 0 : hi + (kr[r] << 20), __double2loint(dd));
+            if (r < nvalid) orow[r * I8_N] = res;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < I8_RPT; ++r)
+            if (r < nvalid) orow[r * I8_N] = i8_scale_slow(sprime(r), kr[r]);
+        }
+        if (warp == EPI0 && lane == 0) I8_TRACE(it, 14 + c);
       }
       if (warp == EPI0 && lane == 0) I8_TRACE(it, 6);
-      i8_arrive(&sempty[buf]);
     }
   } else if (warp == MMAW) {
     // ---- MMA issuer ---------------------------------------------------------------
@@ -409,30 +517,35 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
         const int ab = chunk_ctr & 1;
         if (chunk_ctr >= 2) i8_wait(&aempty[ab], (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
         tc_fence_after();
+        if (lane == 0) I8_TRACE(it, 8 + 2 * c);
         if (!(dbg & 1)) {
-          const uint32_t dacc = tmem + (uint32_t)(I8_ACC0 + ab * I8_ACCBUF);
+          // uz is a kernel parameter equal to 0: deriving every operand from it
+          // keeps the addresses in uniform registers (UIADD3 from the constant
+          // bank) instead of materialising 50+ immediates through vector registers.
+          const uint32_t dacc = uz + (uint32_t)(I8_ACC0 + ab * I8_ACCBUF);
           const uint64_t desc0 = umma_desc_sw128(xbase + (uint32_t)(buf * I8_XBUF_BYTES + c * I8_CHUNK * 128));
-          // all 26 digit pairs x 4 k-steps, fully unrolled: (p, q, ks) are
-          // compile-time, so each MMA is one descriptor add + UTCIMMA
+          // k-step outermost: consecutive MMAs hit different level accumulators,
+          // and each k-step needs only 6 A addresses, 6 B descriptors, 7 D addresses
 #pragma unroll
-          for (int p = 1; p <= I8_ND; ++p) {
+          for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-            for (int q = 1; q <= I8_ND; ++q) {
-              if (p + q > I8_LMAX) continue;
-              const int l = p + q;
-              // first pair of level l in this (p, q) order overwrites the accumulator
-              const bool first = (p == 1) || (l > I8_ND + 1 && p == l - I8_ND);
-              const uint32_t idesc = idesc_i8(q == 1, p == 1);  // A = C digits (q), B = X digits (p)
+            for (int p = 1; p <= I8_ND; ++p) {
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {
+              for (int q = 1; q <= I8_ND; ++q) {
+                if (p + q > I8_LMAX) continue;
+                const int l = p + q;
+                // the first pair of level l (at k-step 0) overwrites the accumulator
+                const bool first = ks == 0 && ((p == 1) || (l > I8_ND + 1 && p == l - I8_ND));
+                const uint32_t idesc = uz + idesc_i8(q == 1, p == 1);  // A = C digits (q), B = X digits (p)
                 const uint64_t bdesc = desc0 + (uint64_t)(((p - 1) * I8_PLANE_BYTES + 32 * ks) >> 4);
-                const uint32_t atm = tmem + (uint32_t)(32 * (q - 1) + 8 * ks);
-                umma_i8_ts(dacc + (uint32_t)((l - 2) * I8_CHUNK), atm, bdesc, idesc, (first && ks == 0) ? 0u : 1u);
+                const uint32_t atm = uz + (uint32_t)(32 * (q - 1) + 8 * ks);
+                umma_i8_ts(dacc + (uint32_t)((l - 2) * I8_CHUNK), atm, bdesc, idesc, first ? 0u : 1u);
               }
             }
           }
         }
         umma_commit_elect(&afull[ab]);
+        if (lane == 0) I8_TRACE(it, 9 + 2 * c);
         __syncwarp();
       }
       umma_commit_elect(&xempty[buf]);
@@ -441,6 +554,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
     }
   } else {
     // ---- slicer warps: rows 16w .. 16w+15 of each tile, from the smem stage ----
+    const int kbias = fT - 1072;  // k = e + fT - 50 with e = bc - 1022
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
       i8_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));
@@ -476,20 +590,18 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
           for (int u = 0; u < RG; ++u) {
             const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
             const int bexp = (int)(m[u] >> 20);  // biased exponent of max|x|
-            // a non-finite row cannot be split: zero digits, NaN scale (-> NaN row,
-            // what x T gives in fp64)
+            // Branch-free (so the RG rows interleave): with the biased exponent
+            // clamped to bc, scale = 2^(47-e) and rs = 2^(e-30), e = bc - 1022.
+            //  * zero row: any finite scale (the digits are 0 and X^A = X exactly);
+            //  * tiny row (max|x| < 2^-977): clamped at bc = 46, the row keeps
+            //    47 - (46 - bexp) bits instead of overflowing the scale;
+            //  * non-finite row: the digits are don't-care and rs = NaN makes the
+            //    row NaN, what x T gives in fp64.
             const bool finite_row = bexp != 0x7ff;
-            const int e = (m[u] == 0) ? 0 : bexp - 1022;  // max|x| < 2^e
-            // 2^(47-e) and 2^(e-30) straight from the biased exponent (normal range);
-            // zero, tiny (bexp < 46) and non-finite rows take the general path
-            double scale, rs;
-            if (finite_row && bexp >= 46) {
-              scale = __longlong_as_double((long long)(2092 - bexp) << 52);
-              rs = __longlong_as_double((long long)(bexp - 29) << 52);
-            } else {
-              scale = finite_row ? pow2(47 - e) : 0.0;
-              rs = finite_row ? pow2(e - 30) : __longlong_as_double(0x7ff8000000000000ll);
-            }
+            const int bc = (m[u] == 0) ? 1023 : max(bexp, 46);
+            const double scale = __longlong_as_double((long long)(2092 - bc) << 52);
+            const double rs = finite_row ? __longlong_as_double((long long)(bc - 29) << 52)
+                                         : __longlong_as_double(0x7ff8000000000000ll);
             // round(x 2^(47-e)) as a 48-bit integer: the low word of fma(x, s, 1.5 2^52)
             // is the low word of the integer, the high word is offset by 0x43380000
             uint32_t vlo[4], vhi[4];
@@ -519,13 +631,14 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ C /* 
             two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 1u, 0u, w[4], w[5]);  // bytes 1, 0
 #pragma unroll
             for (int p = 0; p < I8_ND; ++p) *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = w[p];
-            if (lane == 0) rscale[buf * I8_TILE + r] = rs;
+            if (lane == 0) rinfo[(int)(it % (2 * I8_NBUF)) * I8_TILE + r] = finite_row ? bc + kbias : INT_MIN;
           }
         }
       }
       fence_proxy_async();
       if (warp == 0 && lane == 0) I8_TRACE(it, 2);
       i8_arrive(&xfull[buf]);
+      i8_arrive(&rfull[it % (2 * I8_NBUF)]);
       i8_arrive(&sempty[buf]);
     }
   }

@@ -223,7 +223,7 @@ cudaError_t launch_anomaly_i8(const enkf_plan* p, const double* X, const double*
   const int64_t ntiles = (n_rows + I8_TILE - 1) / I8_TILE;
   const int grid = (int)(ntiles < p->num_sms ? ntiles : p->num_sms);
   if (grid < 1) return cudaSuccess;
-  anomaly_i8_kernel<<<grid, I8_THREADS, smem, s>>>(X, T, XA, n_rows, p->i8_dbg);
+  anomaly_i8_kernel<<<grid, I8_THREADS, smem, s>>>(X, T, XA, n_rows, p->i8_dbg, 0u);
   return cudaGetLastError();
 }
 
