@@ -57,7 +57,7 @@ constexpr int I8_ACCBUF = I8_NLEV * I8_CHUNK;
 
 __host__ __device__ inline size_t anomaly_i8_smem_bytes() {
   return 1024 /*align slack*/ + I8_NBUF * ((size_t)I8_XBUF_BYTES + (size_t)I8_STAGE_BYTES) +
-         I8_NBUF * I8_TILE * sizeof(double) + 512;
+         I8_NBUF * I8_TILE * sizeof(double) + 2 * I8_NBUF * I8_SLICE_WARPS * sizeof(int) + 512;
 }
 // exact int32 -> double: 2^52 + 2^31 trick (one LOP + one DADD)
 __device__ __forceinline__ double i32_to_f64(uint32_t a) {
@@ -70,6 +70,9 @@ __device__ __forceinline__ double i32_to_f64(uint32_t a) {
 // contiguous 512-byte LDS.128 rows (no bank conflicts).
 __host__ __device__ __forceinline__ int i8_kperm(int w, int b) { return (b < 2 ? 2 * w + b : 64 + 2 * w + b - 2); }
 
+#ifndef I8_ROLE_LAYOUT
+#define I8_ROLE_LAYOUT 0
+#endif
 #ifndef I8_EPI_MODE
 #define I8_EPI_MODE 0
 #endif
@@ -97,6 +100,20 @@ __device__ __forceinline__ void i8_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 #endif
+}
+__device__ __forceinline__ void i8_wait_a(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      " @!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+__device__ __forceinline__ void i8_arrive_a(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
 }
 // one arrival per warp (barrier counts are in warps) or per thread
 __device__ __forceinline__ void i8_arrive(uint64_t* bar) {
@@ -247,8 +264,12 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef I8_TRACE_ON  // profiling builds only (tools/probe/i8_trace.py builds the "trace" variant)
 #define I8_TRACE(it, ev) \
   do { if ((dbg & 8) && blockIdx.x == 0 && (it) < I8_TRACE_TILES) g_i8_trace[(it)][(ev)] = gtime(); } while (0)
+#else
+#define I8_TRACE(it, ev) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(I8_THREADS, 1)
 anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
@@ -263,7 +284,9 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
   // per-row exponent shift k [2*NBUF][32] (X^A = S' 2^k; INT_MIN for non-finite rows),
   // a ring twice the stage depth so the slicers never overwrite a tile the epilogue reads
   int* rinfo = reinterpret_cast<int*>(stage + I8_NBUF * I8_TILE * I8_N);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rinfo + 2 * I8_NBUF * I8_TILE);
+  // [2*NBUF][slicer warp]: 1 if one of that warp's 8 rows needs the slow scaling path
+  int* rflag = rinfo + 2 * I8_NBUF * I8_TILE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rflag + 2 * I8_NBUF * I8_SLICE_WARPS);
   uint64_t* sfull = bars;                  // [NBUF] TMA -> slicers/epilogue      (count 1 + tx)
   uint64_t* sempty = bars + I8_NBUF;       // [NBUF] slicers -> producer              (count slicer warps)
   uint64_t* xfull = bars + 2 * I8_NBUF;    // [NBUF] slicers -> MMA               (count slicer threads)
@@ -277,11 +300,27 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
   // threads).  Its own ring (depth 8 > the at most 5 tiles the slicers run ahead of
   // the epilogue) keeps the parity waits unambiguous.
   uint64_t* rfull = bars + 4 * I8_NBUF + 8;
+  const uint32_t sfull_a = smem_u32(sfull), sempty_a = smem_u32(sempty), xfull_a = smem_u32(xfull);
+  const uint32_t xempty_a = smem_u32(xempty), afull_a = smem_u32(afull), aempty_a = smem_u32(aempty);
+  const uint32_t rfull_a = smem_u32(rfull);
 
-  constexpr int EPI0 = I8_SLICE_WARPS;                 // first epilogue warp
-  constexpr int MMAW = I8_SLICE_WARPS + I8_EPI_WARPS;  // MMA warp
-  constexpr int TMAW = MMAW + 1;                       // producer warp
+  // Epilogue warps sit at warp ids 4..4+EW-1 (a warp may only touch the TMEM lane
+  // quadrant warp_id % 4).  I8_ROLE_LAYOUT 1 gives the MMA issuer warp 0 (SMSP 0)
+  // and moves slicer 0 to the last warp id, so the MMA warp does not share its
+  // SMSP with a slicer.
+  constexpr int EPI0 = 4;
+  static_assert(I8_SLICE_WARPS == 4, "role layout assumes 4 slicer warps");
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if I8_ROLE_LAYOUT
+  constexpr int MMAW = 0;
+  constexpr int TMAW = EPI0 + I8_EPI_WARPS;
+  const int sw = (warp >= 1 && warp < 4) ? warp : (warp == TMAW + 1 ? 0 : -1);  // slicer index
+#else
+  constexpr int MMAW = EPI0 + I8_EPI_WARPS;
+  constexpr int TMAW = MMAW + 1;
+  const int sw = warp < 4 ? warp : -1;
+#endif
   const int64_t ntiles = (n_rows + I8_TILE - 1) / I8_TILE;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -347,7 +386,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
       for (int64_t it = 0; it < my_tiles; ++it) {
         const int buf = (int)(it % I8_NBUF);
         const int64_t tile = blockIdx.x + it * gridDim.x;
-        if (it >= I8_NBUF) i8_wait(&sempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
+        if (it >= I8_NBUF) i8_wait_a(sempty_a + 8u * (uint32_t)(buf), (uint32_t)(((it / I8_NBUF) - 1) & 1));
         fence_proxy_async();
         const int64_t g0 = tile * I8_TILE;
         const int rows = (int)(n_rows - g0 < I8_TILE ? n_rows - g0 : I8_TILE);
@@ -363,7 +402,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         }
       }
     }
-  } else if (warp >= EPI0 && warp < MMAW) {
+  } else if (warp >= EPI0 && warp < EPI0 + I8_EPI_WARPS) {
     // ---- epilogue warps: thread = output column j = TMEM lane ------------------
     const int quad = warp & 3;            // TMEM lane quadrant this warp may access
     const int half = (warp - EPI0) >> 2;  // which I8_RPT rows of each 16-row chunk
@@ -394,19 +433,19 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
       const int64_t tile = blockIdx.x + it * gridDim.x;
-      i8_wait(&rfull[it % (2 * I8_NBUF)], (uint32_t)((it / (2 * I8_NBUF)) & 1));  // the tile's row exponents
+      i8_wait_a(rfull_a + 8u * (uint32_t)(it % (2 * I8_NBUF)), (uint32_t)((it / (2 * I8_NBUF)) & 1));  // the tile's row exponents
       const int* rk = rinfo + (int)(it % (2 * I8_NBUF)) * I8_TILE;
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
         const int r0 = c * I8_CHUNK + I8_RPT * half;  // first tile row of this thread's I8_RPT
         const int64_t g0 = tile * I8_TILE + r0;
-        i8_wait(&afull[ab], (uint32_t)((chunk_ctr >> 1) & 1));
+        i8_wait_a(afull_a + 8u * (uint32_t)(ab), (uint32_t)((chunk_ctr >> 1) & 1));
         tc_fence_after();
         if (c == 0 && warp == EPI0 && lane == 0) I8_TRACE(it, 5);
         if (warp == EPI0 && lane == 0) I8_TRACE(it, 12 + c);
         if (dbg & 4) {
           tc_fence_before();
-          i8_arrive(&aempty[ab]);
+          i8_arrive_a(aempty_a + 8u * (uint32_t)(ab));
           continue;
         }
         const uint32_t tbase = tmem + ((uint32_t)(32 * quad) << 16) +
@@ -416,7 +455,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         for (int l = 0; l < I8_NLEV; ++l) tmem_ldr<I8_RPT>(tbase + (uint32_t)(l * I8_CHUNK), v[l]);
         tmem_ld_wait();
         tc_fence_before();
-        i8_arrive(&aempty[ab]);  // accumulators copied out: the MMA may reuse them
+        i8_arrive_a(aempty_a + 8u * (uint32_t)(ab));  // accumulators copied out: the MMA may reuse them
         if (dbg & 16) {          // profiling: drain TMEM but skip the recombination and stores
           // ... and burn 128 independent ops of one kind per thread (op = dbg >> 7):
           // 1 DFMA, 2 IMAD, 3 IMAD.WIDE, 4 I2F.F64.S32, 5 DADD, 6 I2F.F64.S64, 7 DMUL
@@ -472,9 +511,10 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
           const int4 k4 = *reinterpret_cast<const int4*>(rk + r0 + r);
           kr[r] = k4.x; kr[r + 1] = k4.y; kr[r + 2] = k4.z; kr[r + 3] = k4.w;
         }
-        bool slow = false;  // rows near the fp64 range limits or non-finite (warp-uniform, rare)
-#pragma unroll
-        for (int r = 0; r < I8_RPT; ++r) slow |= (kr[r] < -1022) | (kr[r] > 961);
+        // rows near the fp64 range limits or non-finite (warp-uniform, rare); the
+        // slicer warp that formed these 8 rows flagged them
+        static_assert(I8_RPT == 8 && I8_TILE / I8_SLICE_WARPS == 8, "epilogue row group = slicer row group");
+        const bool slow = rflag[(int)(it % (2 * I8_NBUF)) * I8_SLICE_WARPS + (r0 >> 3)] != 0;
         auto sprime = [&](int r) {
           const int d2 = (int)v[0][r], d3 = (int)v[1][r], d4 = (int)v[2][r], d5 = (int)v[3][r];
           const int d6 = (int)v[4][r], d7 = (int)v[5][r], d8 = (int)v[6][r];
@@ -510,12 +550,12 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
-      i8_wait(&xfull[buf], (uint32_t)((it / I8_NBUF) & 1));
+      i8_wait_a(xfull_a + 8u * (uint32_t)(buf), (uint32_t)((it / I8_NBUF) & 1));
       tc_fence_after();
       if (lane == 0) I8_TRACE(it, 3);
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
         const int ab = chunk_ctr & 1;
-        if (chunk_ctr >= 2) i8_wait(&aempty[ab], (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
+        if (chunk_ctr >= 2) i8_wait_a(aempty_a + 8u * (uint32_t)(ab), (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
         tc_fence_after();
         if (lane == 0) I8_TRACE(it, 8 + 2 * c);
         if (!(dbg & 1)) {
@@ -557,10 +597,11 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     const int kbias = fT - 1072;  // k = e + fT - 50 with e = bc - 1022
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
-      i8_wait(&sfull[buf], (uint32_t)((it / I8_NBUF) & 1));
-      if (warp == 0 && lane == 0) I8_TRACE(it, 1);
-      if (it >= I8_NBUF) i8_wait(&xempty[buf], (uint32_t)(((it / I8_NBUF) - 1) & 1));
-      if (warp == 0 && lane == 0) I8_TRACE(it, 7);
+      i8_wait_a(sfull_a + 8u * (uint32_t)(buf), (uint32_t)((it / I8_NBUF) & 1));
+      if (sw == 0 && lane == 0) I8_TRACE(it, 1);
+      if (it >= I8_NBUF) i8_wait_a(xempty_a + 8u * (uint32_t)(buf), (uint32_t)(((it / I8_NBUF) - 1) & 1));
+      if (sw == 0 && lane == 0) I8_TRACE(it, 7);
+      bool wslow = false;
       unsigned char* planes = xdig + buf * I8_XBUF_BYTES;
       const double* xs = stage + buf * I8_TILE * I8_N;
       if (!(dbg & 2)) {
@@ -571,7 +612,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
           uint32_t m[RG];
 #pragma unroll
           for (int u = 0; u < RG; ++u) {
-            const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
+            const int r = (I8_TILE / I8_SLICE_WARPS) * sw + rb + u;
             // k = 2l, 2l+1 and 64+2l, 65+2l (i8_kperm): two conflict-free 512 B rows
             const double2 a0 = *reinterpret_cast<const double2*>(xs + r * I8_N + 2 * lane);
             const double2 a1 = *reinterpret_cast<const double2*>(xs + r * I8_N + 64 + 2 * lane);
@@ -588,7 +629,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
           for (int u = 0; u < RG; ++u) m[u] = __reduce_max_sync(0xffffffffu, m[u]);  // one REDUX per row
 #pragma unroll
           for (int u = 0; u < RG; ++u) {
-            const int r = (I8_TILE / I8_SLICE_WARPS) * warp + rb + u;
+            const int r = (I8_TILE / I8_SLICE_WARPS) * sw + rb + u;
             const int bexp = (int)(m[u] >> 20);  // biased exponent of max|x|
             // Branch-free (so the RG rows interleave): with the biased exponent
             // clamped to bc, scale = 2^(47-e) and rs = 2^(e-30), e = bc - 1022.
@@ -631,15 +672,18 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
             two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 1u, 0u, w[4], w[5]);  // bytes 1, 0
 #pragma unroll
             for (int p = 0; p < I8_ND; ++p) *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = w[p];
-            if (lane == 0) rinfo[(int)(it % (2 * I8_NBUF)) * I8_TILE + r] = finite_row ? bc + kbias : INT_MIN;
+            const int kv = finite_row ? bc + kbias : INT_MIN;
+            wslow |= (kv < -1022) | (kv > 961);  // outside the exponent-field fast path
+            if (lane == 0) rinfo[(int)(it % (2 * I8_NBUF)) * I8_TILE + r] = kv;
           }
         }
       }
+      if (lane == 0) rflag[(int)(it % (2 * I8_NBUF)) * I8_SLICE_WARPS + sw] = wslow;
       fence_proxy_async();
-      if (warp == 0 && lane == 0) I8_TRACE(it, 2);
-      i8_arrive(&xfull[buf]);
-      i8_arrive(&rfull[it % (2 * I8_NBUF)]);
-      i8_arrive(&sempty[buf]);
+      if (sw == 0 && lane == 0) I8_TRACE(it, 2);
+      i8_arrive_a(xfull_a + 8u * (uint32_t)(buf));
+      i8_arrive_a(rfull_a + 8u * (uint32_t)(it % (2 * I8_NBUF)));
+      i8_arrive_a(sempty_a + 8u * (uint32_t)(buf));
     }
   }
   tc_fence_before();
