@@ -15,6 +15,7 @@
 #include "anomaly_i8.cuh"
 #include "localized.cuh"
 #include "l96.cuh"
+#include "gram_i8.cuh"
 
 using namespace enkf;
 
@@ -30,6 +31,12 @@ struct enkf_plan {
   bool anomaly_i8 = true;      // tensor-core (int8 digit) anomaly update, N == 128
   int i8_dbg = 0;              // profiling-only role skips (ENKF_I8_DBG)
   bool levels_blocked = true;  // blocked (LB levels per barrier) Sherman-Morrison recursion
+  bool gram_i8 = false;        // tensor-core (int8 digit) Gram, N == 128 analysis mode (opt-in: ENKF_GRAM=i8)
+  int g8_groups = 0;           // groups of 4 CTAs over the observation rows
+  int64_t g8_rows = 0;         // observation rows per group (multiple of 64)
+  double* g8_rinv = nullptr;   // [n_obs + 64] 1/r
+  unsigned long long* g8_meta = nullptr;  // [384] sampled column maxima, then the overflow flag
+  double* g8_partial = nullptr;           // [groups][4][128][64]
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
   int g128_cpb_vv = 1, g128_cpb_vd = 1;     // gram128: CTAs for the V'V / V'D blocks
@@ -118,7 +125,7 @@ cudaError_t launch_gram_ws_t(const enkf_plan* p, const double* X, const double* 
     if (e != cudaSuccess) return e;
     kern<<<p->g128_cpb_vv + p->g128_cpb_vd, W_THREADS, smem, s>>>(
         X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv, p->g128_rows_vv, p->g128_rows_vd,
-        p->partial, p->dstatus);
+        p->partial, p->dstatus, nullptr);
     return cudaGetLastError();
   }
   const int ld = padded_ld(W_TILE);  // operand tiles are 128 wide whatever n is
@@ -136,10 +143,15 @@ bool use_ws(const enkf_plan* p, const void* a, const void* b) {
   return p->use_ws && (p->n % 2 == 0) && aligned16(a) && aligned16(b);
 }
 
-cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, const double* Y,
+cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
+                           const double* r, double* gram, cudaStream_t s);
+
+cudaError_t launch_gram(enkf_plan* p, bool analysis, const double* X, const double* Y,
                         const int64_t* idx, const double* r, double* gram, cudaStream_t s) {
   const int n = p->n;
   if (p->n_obs == 0) return cudaMemsetAsync(gram, 0, sizeof(double) * n * 2 * n, s);
+  if (analysis && n == G8_N && p->gram_i8 && p->use_128 && use_ws(p, X, Y))
+    return launch_gram_i8(p, X, Y, idx, r, gram, s);
   if (use_ws(p, X, Y)) {
     cudaError_t e = analysis ? launch_gram_ws_t<true>(p, X, Y, idx, r, s)
                              : launch_gram_ws_t<false>(p, X, Y, idx, r, s);
@@ -149,7 +161,7 @@ cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, cons
     const int64_t count = (int64_t)n * 2 * n;
     if (n == W_TILE && p->use_128)
       gram128_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, p->g128_cpb_vv,
-                                                                     p->g128_cpb_vd, svv, svd, gram);
+                                                                     p->g128_cpb_vd, svv, svd, gram, nullptr);
     else
       gram_ws_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
                                                                     svv, svd, gram);
@@ -164,6 +176,48 @@ cudaError_t launch_gram(const enkf_plan* p, bool analysis, const double* X, cons
   const double svd = analysis ? 1.0 / std::sqrt((double)(n - 1)) : 1.0;
   const int64_t count = (int64_t)n * 2 * n;
   gram_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, p->splits, n, svv, svd, gram);
+  return cudaGetLastError();
+}
+
+// int8 tensor-core Gram (gram_i8.cuh): 1/r, sampled column scales, the digit
+// kernel, the reduce, and the FP64 gram128 pass gated on the overflow flag.
+cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
+                           const double* r, double* gram, cudaStream_t s) {
+  const int n = p->n;
+  cudaError_t e = cudaSuccess;
+  const int64_t n_pad = p->n_obs + 64;
+  if (!p->g8_rinv) {
+    e = cudaMalloc(&p->g8_rinv, sizeof(double) * (size_t)n_pad);
+    if (e == cudaSuccess) e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (3 * G8_N + 2));
+    if (e == cudaSuccess)
+      e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS);
+    if (e != cudaSuccess) return e;
+  }
+  int* overflow = reinterpret_cast<int*>(p->g8_meta + 3 * G8_N);
+  if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (3 * G8_N + 2), s)) != cudaSuccess) return e;
+  const int rgrid = (int)std::min<int64_t>((n_pad + 255) / 256, (int64_t)p->num_sms * 8);
+  rinv_kernel<<<rgrid, 256, 0, s>>>(r, p->g8_rinv, p->n_obs, n_pad, p->dstatus);
+  gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, p->g8_rinv, p->n_state, p->n_obs, p->g8_meta);
+  const size_t smem = gram_i8_smem_bytes();
+  if ((e = cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  gram_i8_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(X, Y, idx, p->g8_rinv, p->g8_meta, p->n_state, p->n_obs,
+                                                            p->g8_rows, p->g8_partial, overflow, p->dstatus, 0u);
+  const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
+  gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
+  // FP64 fallback, a no-op unless an element fell outside the sampled scales
+  {
+    const int ld = padded_ld(W_TILE);
+    const size_t gsmem = gram128_smem_bytes(ld);
+    auto kern = gram128_kernel<true>;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem)) != cudaSuccess)
+      return e;
+    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, W_THREADS, gsmem, s>>>(X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv,
+                                                                   p->g128_rows_vv, p->g128_rows_vd, p->partial,
+                                                                   p->dstatus, overflow);
+    gram128_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->partial, p->g128_cpb_vv, p->g128_cpb_vd, svv,
+                                                                 svd, gram, overflow);
+  }
   return cudaGetLastError();
 }
 
@@ -489,6 +543,13 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
+  if (const char* env = getenv("ENKF_GRAM")) p->gram_i8 = (strcmp(env, "i8") == 0);
+  p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
+  {
+    int64_t rr = (n_obs + p->g8_groups - 1) / p->g8_groups;
+    rr = (rr + G8_KB - 1) / G8_KB * G8_KB;
+    p->g8_rows = rr < G8_KB ? G8_KB : rr;
+  }
 
   // gram128 split: the V'V CTAs do 3/4 of the DMMA work of the V'D CTAs (and
   // lighter transforms), so they get fewer CTAs with more rows each.
@@ -552,6 +613,9 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->locD);
   cudaFree(p->locZ);
   cudaFree(p->l96ws);
+  cudaFree(p->g8_rinv);
+  cudaFree(p->g8_meta);
+  cudaFree(p->g8_partial);
   cudaFree(p->cyc_status);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
@@ -901,6 +965,9 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
   return ENKF_OK;
 }
 
+__attribute__((visibility("default"))) int32_t enkf_debug_g8_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, enkf::g_g8_trace, sizeof(enkf::g_g8_trace)) == cudaSuccess ? 0 : 5;
+}
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {

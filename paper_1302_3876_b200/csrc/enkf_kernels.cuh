@@ -679,7 +679,10 @@ __global__ void __launch_bounds__(W_THREADS, 1)
 gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                const int64_t* __restrict__ idx, const double* __restrict__ r,
                int64_t n_state, int64_t n_obs, int ld, int cpb_vv, int64_t rows_vv,
-               int64_t rows_vd, double* __restrict__ partial, DevStatus* __restrict__ status) {
+               int64_t rows_vd, double* __restrict__ partial, DevStatus* __restrict__ status,
+               const int* __restrict__ gate = nullptr) {
+  // gate (the int8 Gram's overflow flag): run only as its FP64 fallback
+  if (gate != nullptr && *gate == 0) return;
   constexpr int n = 128;
   extern __shared__ __align__(128) unsigned char psm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -902,7 +905,9 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 // Fixed-order reduction for gram128: V'V entries (upper triangle computed,
 // lower mirrored) from the cpb_vv V'V CTAs, V'D entries from the V'D CTAs.
 __global__ void gram128_reduce(const double* __restrict__ partial, int cpb_vv, int cpb_vd,
-                               double s_vv, double s_vd, double* __restrict__ gram) {
+                               double s_vv, double s_vd, double* __restrict__ gram,
+                               const int* __restrict__ gate = nullptr) {
+  if (gate != nullptr && *gate == 0) return;
   constexpr int n = 128;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * 2 * n) return;

@@ -406,3 +406,48 @@ def test_tensor_core_anomaly_zero_spread_and_nonfinite():
     mask[3] = False
     ref = x2[mask] @ t.cpu().numpy()
     assert rel_err(o[mask], ref) <= 1e-12
+
+
+# ---------------------------------------------------------------- opt-in int8 Gram
+def _gram_with(mode, heavy=False):
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys, ctypes
+import numpy as np, torch
+sys.path.insert(0, os.getcwd())
+from paper_1302_3876_b200 import _native
+heavy = int(sys.argv[1])
+dev = torch.device("cuda", 0); lib = _native.lib(); s = torch.cuda.current_stream().cuda_stream
+n, ns, no = 128, 1 << 17, 1 << 15
+g = torch.Generator(device=dev); g.manual_seed(11)
+x = torch.randn((ns, 1), dtype=torch.float64, device=dev, generator=g) + (0.5 + 1.5 * torch.rand((ns, 1), dtype=torch.float64, device=dev, generator=g)) * torch.randn((ns, n), dtype=torch.float64, device=dev, generator=g)
+idx = torch.sort(torch.randperm(ns, device=dev, generator=g)[:no]).values
+y = x[idx].mean(dim=1, keepdim=True) + torch.randn((no, n), dtype=torch.float64, device=dev, generator=g)
+if heavy:
+    y[no // 3, 5] = 1e6
+r = 0.25 + 0.75 * torch.rand((no,), dtype=torch.float64, device=dev, generator=g)
+plan = _native.Plan(ns, no, n, 0)
+gram = torch.empty((n, 2 * n), dtype=torch.float64, device=dev)
+assert lib.enkf_ism_gram_f64(plan.handle, x.data_ptr(), y.data_ptr(), idx.data_ptr(), r.data_ptr(), gram.data_ptr(), s) == 0
+st = _native.EnkfStatus()
+assert lib.enkf_plan_sync_status(plan.handle, s, ctypes.byref(st)) == 0
+np.save(sys.argv[2], gram.cpu().numpy())
+'''
+    import tempfile
+    out = tempfile.mktemp(suffix=".npy")
+    env = dict(os.environ, ENKF_GRAM=mode)
+    subprocess.run([sys.executable, "-c", code, str(int(heavy)), out], env=env, check=True, timeout=300)
+    return np.load(out)
+
+
+@pytest.mark.parametrize("heavy", [False, True])
+def test_int8_gram_matches_fp64_gram(heavy):
+    """ENKF_GRAM=i8: the exact-digit tcgen05 Gram agrees with the FP64 DMMA Gram to
+    rounding level; a heavy-tailed element outside the sampled scales takes the
+    device-gated FP64 fallback (then the two are identical)."""
+    a, b = _gram_with("fp64", heavy), _gram_with("i8", heavy)
+    assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
+    tol = 0.0 if heavy else 1e-13
+    assert np.abs(a - b).max() <= tol * np.abs(a).max()
