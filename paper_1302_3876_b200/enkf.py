@@ -165,6 +165,20 @@ def innovations(obs: ObservationBatch, h: SelectionOperator, x):
     return out if dev_in else out.cpu().numpy()
 
 
+_PINNED_RESULT_BYTES = 64 << 20
+
+
+def _host_result(shape) -> np.ndarray:
+    """A new C-order float64 result array.  Large results live in page-locked
+    memory from torch's caching host allocator, so the device->host copy runs at
+    full PCIe speed straight into the caller's array (fresh pageable pages
+    fault at a few GB/s); the block returns to the cache when the array dies."""
+    nbytes = int(np.prod(shape)) * 8
+    if nbytes >= _PINNED_RESULT_BYTES:
+        return torch.empty(tuple(shape), dtype=torch.float64, pin_memory=True).numpy()
+    return np.empty(shape, dtype=np.float64)
+
+
 def _check_obs_shapes(nobs: int, nens: int, perturbed_shape, r_shape):
     if len(perturbed_shape) != 2 or tuple(perturbed_shape) != (nobs, nens):
         raise ValueError(f"perturbed observations have shape {tuple(perturbed_shape)}, "
@@ -241,7 +255,7 @@ def analysis_step(
     yh = np.ascontiguousarray(perturbed, dtype=np.float64)
     rh = np.ascontiguousarray(r_host, dtype=np.float64)
     idxh = None if h.indices is None else np.ascontiguousarray(h.indices, dtype=np.int64)
-    out = np.empty_like(xh)
+    out = _host_result(xh.shape)
     st = _native.EnkfStatus()
     with plan.lock:
         code = _native.lib().enkf_analysis_host_f64(
