@@ -59,10 +59,6 @@ __host__ __device__ inline size_t anomaly_i8_smem_bytes() {
   return 1024 /*align slack*/ + I8_NBUF * ((size_t)I8_XBUF_BYTES + (size_t)I8_STAGE_BYTES) +
          I8_NBUF * I8_TILE * sizeof(double) + 2 * I8_NBUF * I8_SLICE_WARPS * sizeof(int) + 512;
 }
-// exact int32 -> double: 2^52 + 2^31 trick (one LOP + one DADD)
-__device__ __forceinline__ double i32_to_f64(uint32_t a) {
-  return __hiloint2double(0x43300000, (int)(a ^ 0x80000000u)) - 4503601774854144.0;
-}
 
 // K order of the digit planes: word w of a plane row holds k = 2w, 2w+1, 64+2w,
 // 65+2w (bytes 0..3).  Any permutation of k applied to both operands leaves the
@@ -70,37 +66,9 @@ __device__ __forceinline__ double i32_to_f64(uint32_t a) {
 // contiguous 512-byte LDS.128 rows (no bank conflicts).
 __host__ __device__ __forceinline__ int i8_kperm(int w, int b) { return (b < 2 ? 2 * w + b : 64 + 2 * w + b - 2); }
 
-#ifndef I8_ROLE_LAYOUT
-#define I8_ROLE_LAYOUT 0
-#endif
-#ifndef I8_EPI_MODE
-#define I8_EPI_MODE 0
-#endif
-#ifndef I8_CVT_MAGIC
-#define I8_CVT_MAGIC 0
-#endif
-#ifndef I8_WAIT_HINT
-#define I8_WAIT_HINT 1
-#endif
 #ifndef I8_WARP_ARRIVE
 #define I8_WARP_ARRIVE 0
 #endif
-// mbarrier wait used by this kernel (variant selectable at compile time)
-__device__ __forceinline__ void i8_wait(uint64_t* bar, uint32_t parity) {
-#if I8_WAIT_HINT
-  mbar_wait(bar, parity);
-#else
-  asm volatile(
-      "{\n"
-      " .reg .pred P1;\n"
-      "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-#endif
-}
 __device__ __forceinline__ void i8_wait_a(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -274,7 +242,11 @@ __device__ __forceinline__ unsigned long long gtime() {
 __global__ void __launch_bounds__(I8_THREADS, 1)
 anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
                   double* __restrict__ XA, int64_t n_rows, int dbg, uint32_t uz /* = 0 */) {
-  // dbg (profiling only): bit0 skip MMAs, bit1 skip slicing, bit2 skip epilogue math/IO
+  // dbg (profiling only): bit0 skip MMAs, bit1 skip slicing, bit2 skip the epilogue,
+  // bit4 drain TMEM but skip the recombination, bit5 stores into an L2-resident window.
+  // Measured with these (tools/probe/i8_trace.py): FP64 arithmetic (DFMA/DADD/DMUL)
+  // issued by other warps slows the int8 MMAs roughly in proportion to its count,
+  // integer ops and int->fp64 conversions do not.
   extern __shared__ __align__(1024) unsigned char i8sm_raw[];
   // realign by a byte offset (not an integer round trip) so the compiler keeps
   // the shared address space and emits LDS/STS, not generic LD/ST
@@ -305,22 +277,14 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
   const uint32_t rfull_a = smem_u32(rfull);
 
   // Epilogue warps sit at warp ids 4..4+EW-1 (a warp may only touch the TMEM lane
-  // quadrant warp_id % 4).  I8_ROLE_LAYOUT 1 gives the MMA issuer warp 0 (SMSP 0)
-  // and moves slicer 0 to the last warp id, so the MMA warp does not share its
-  // SMSP with a slicer.
+  // quadrant warp_id % 4); slicers 0..3, then the MMA issuer and the producer.
+  // (Giving the MMA issuer an SMSP without a slicer was measured 20% slower.)
   constexpr int EPI0 = 4;
   static_assert(I8_SLICE_WARPS == 4, "role layout assumes 4 slicer warps");
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-#if I8_ROLE_LAYOUT
-  constexpr int MMAW = 0;
-  constexpr int TMAW = EPI0 + I8_EPI_WARPS;
-  const int sw = (warp >= 1 && warp < 4) ? warp : (warp == TMAW + 1 ? 0 : -1);  // slicer index
-#else
   constexpr int MMAW = EPI0 + I8_EPI_WARPS;
   constexpr int TMAW = MMAW + 1;
-  const int sw = warp < 4 ? warp : -1;
-#endif
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int sw = warp < 4 ? warp : -1;  // slicer index
   const int64_t ntiles = (n_rows + I8_TILE - 1) / I8_TILE;
   const int64_t my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
@@ -457,39 +421,6 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         tc_fence_before();
         i8_arrive_a(aempty_a + 8u * (uint32_t)(ab));  // accumulators copied out: the MMA may reuse them
         if (dbg & 16) {          // profiling: drain TMEM but skip the recombination and stores
-          // ... and burn 128 independent ops of one kind per thread (op = dbg >> 7):
-          // 1 DFMA, 2 IMAD, 3 IMAD.WIDE, 4 I2F.F64.S32, 5 DADD, 6 I2F.F64.S64, 7 DMUL
-          const int op = (dbg >> 7) & 31;
-          const int iters = (dbg >> 12) ? (dbg >> 12) : 32;  // x4 independent ops each
-          if (op == 1 || op == 5 || op == 7) {
-            double a0 = (double)v[0][0], a1 = (double)v[1][0], a2 = (double)v[2][0], a3 = (double)v[3][0];
-#pragma unroll 4
-            for (int i = 0; i < iters; ++i) {
-              if (op == 1) { a0 = fma(a0, 1.0000001, 0.5); a1 = fma(a1, 1.0000001, 0.5); a2 = fma(a2, 1.0000001, 0.5); a3 = fma(a3, 1.0000001, 0.5); }
-              if (op == 5) { a0 = a0 + 0.5; a1 = a1 + 0.5; a2 = a2 + 0.5; a3 = a3 + 0.5; }
-              if (op == 7) { a0 = a0 * 1.0000001; a1 = a1 * 1.0000001; a2 = a2 * 1.0000001; a3 = a3 * 1.0000001; }
-            }
-            if (a0 + a1 + a2 + a3 == 1234.5) XA[0] = 0.0;
-          } else if (op == 2 || op == 3) {
-            uint32_t a0 = v[0][0], a1 = v[1][0], a2 = v[2][0], a3 = v[3][0];
-            long long w0 = a0, w1 = a1, w2 = a2, w3 = a3;
-#pragma unroll 4
-            for (int i = 0; i < 32; ++i) {
-              if (op == 2) { a0 = a0 * 3u + 7u; a1 = a1 * 3u + 7u; a2 = a2 * 3u + 7u; a3 = a3 * 3u + 7u; }
-              if (op == 3) { w0 = (long long)(int)a0 * 65536 + w0; w1 = (long long)(int)a1 * 65536 + w1;
-                             w2 = (long long)(int)a2 * 65536 + w2; w3 = (long long)(int)a3 * 65536 + w3; }
-            }
-            if (a0 + a1 + a2 + a3 + (uint32_t)(w0 ^ w1 ^ w2 ^ w3) == 12345u) XA[0] = 0.0;
-          } else if (op == 4 || op == 6) {
-            unsigned long long acc = 0;
-#pragma unroll 8
-            for (int i = 0; i < 128; ++i) {
-              const uint32_t u = v[i & 7][0] + (uint32_t)i;
-              acc ^= (unsigned long long)__double_as_longlong((op == 4) ? __int2double_rn((int)u)
-                                                                        : (double)((long long)u << 20));
-            }
-            if (acc == 12345ull) XA[0] = 0.0;
-          }
           if (v[0][0] == 0x7fffffffu) XA[0] = 0.0;
           continue;
         }

@@ -801,22 +801,24 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                                           : make_double2(0.0, 0.0);
           }
           sx[u] = (xv[u][0].x + xv[u][0].y) + (xv[u][1].x + xv[u][1].y);
-          sy[u] = checker ? (yv[u][0].x + yv[u][0].y) + (yv[u][1].x + yv[u][1].y) : 0.0;
+          if (checker) {  // non-finite inputs: integer test of the exponent bits (no FP64 work)
+            uint32_t ex = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t e0 = (uint32_t)__double2hiint(xv[u][h].x), e1 = (uint32_t)__double2hiint(xv[u][h].y);
+              const uint32_t e2 = (uint32_t)__double2hiint(yv[u][h].x), e3 = (uint32_t)__double2hiint(yv[u][h].y);
+              ex |= ((e0 & 0x7ff00000u) == 0x7ff00000u) | ((e1 & 0x7ff00000u) == 0x7ff00000u) |
+                    ((e2 & 0x7ff00000u) == 0x7ff00000u) | ((e3 & 0x7ff00000u) == 0x7ff00000u);
+            }
+            if (ex) flags |= FLAG_NONFINITE;
+          }
         }
-        if (ANALYSIS || checker) {
+        (void)sy;
+        if (ANALYSIS) {
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
             for (int u = 0; u < RPI; ++u) sx[u] += __shfl_xor_sync(0xffffffffu, sx[u], o);
-        }
-        if (checker) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int u = 0; u < RPI; ++u) sy[u] += __shfl_xor_sync(0xffffffffu, sy[u], o);
-#pragma unroll
-          for (int u = 0; u < RPI; ++u)
-            if (valid[u] && !(isfinite(sx[u]) && isfinite(sy[u]))) flags |= FLAG_NONFINITE;
         }
 #pragma unroll
         for (int u = 0; u < RPI; ++u) {
