@@ -30,7 +30,13 @@ namespace enkf {
 constexpr int I8_N = 128;         // ensemble size handled by this kernel
 constexpr int I8_TILE = 32;       // X rows per tile
 constexpr int I8_NBUF = 4;        // pipeline depth (raw X stages and digit buffers)
-constexpr int I8_CHUNK = 16;      // rows per MMA (N of the instruction)
+#ifndef I8_CHUNK_ROWS
+#define I8_CHUNK_ROWS 16
+#endif
+constexpr int I8_CHUNK = I8_CHUNK_ROWS;  // rows per MMA (N of the instruction)
+// TMEM: 192 columns of T digits + accumulators: two 16-row chunk buffers, or one
+// 32-row buffer (N = 32 halves the MMA count; the epilogue drains before reuse)
+constexpr int I8_ABUF = I8_CHUNK == 16 ? 2 : 1;
 constexpr int I8_ND = 6;          // byte digits per value
 constexpr int I8_LMAX = 8;        // keep digit pairs with p + q <= 8
 constexpr int I8_NLEV = I8_LMAX - 1;  // levels 2..8
@@ -400,10 +406,10 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
       i8_wait_a(rfull_a + 8u * (uint32_t)(it % (2 * I8_NBUF)), (uint32_t)((it / (2 * I8_NBUF)) & 1));  // the tile's row exponents
       const int* rk = rinfo + (int)(it % (2 * I8_NBUF)) * I8_TILE;
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
-        const int ab = chunk_ctr & 1;
+        const int ab = chunk_ctr % I8_ABUF;
         const int r0 = c * I8_CHUNK + I8_RPT * half;  // first tile row of this thread's I8_RPT
         const int64_t g0 = tile * I8_TILE + r0;
-        i8_wait_a(afull_a + 8u * (uint32_t)(ab), (uint32_t)((chunk_ctr >> 1) & 1));
+        i8_wait_a(afull_a + 8u * (uint32_t)(ab), (uint32_t)((chunk_ctr / I8_ABUF) & 1));
         tc_fence_after();
         if (c == 0 && warp == EPI0 && lane == 0) I8_TRACE(it, 5);
         if (warp == EPI0 && lane == 0) I8_TRACE(it, 12 + c);
@@ -444,7 +450,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         }
         // rows near the fp64 range limits or non-finite (warp-uniform, rare); the
         // slicer warp that formed these 8 rows flagged them
-        static_assert(I8_RPT == 8 && I8_TILE / I8_SLICE_WARPS == 8, "epilogue row group = slicer row group");
+        static_assert(I8_TILE / I8_SLICE_WARPS == 8 && 8 % I8_RPT == 0, "epilogue rows within one slicer row group");
         const bool slow = rflag[(int)(it % (2 * I8_NBUF)) * I8_SLICE_WARPS + (r0 >> 3)] != 0;
         auto sprime = [&](int r) {
           const int d2 = (int)v[0][r], d3 = (int)v[1][r], d4 = (int)v[2][r], d5 = (int)v[3][r];
@@ -485,8 +491,9 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
       tc_fence_after();
       if (lane == 0) I8_TRACE(it, 3);
       for (int c = 0; c < I8_TILE / I8_CHUNK; ++c, ++chunk_ctr) {
-        const int ab = chunk_ctr & 1;
-        if (chunk_ctr >= 2) i8_wait_a(aempty_a + 8u * (uint32_t)(ab), (uint32_t)(((chunk_ctr >> 1) - 1) & 1));
+        const int ab = chunk_ctr % I8_ABUF;
+        if (chunk_ctr >= I8_ABUF)
+          i8_wait_a(aempty_a + 8u * (uint32_t)(ab), (uint32_t)(((chunk_ctr / I8_ABUF) - 1) & 1));
         tc_fence_after();
         if (lane == 0) I8_TRACE(it, 8 + 2 * c);
         if (!(dbg & 1)) {
@@ -536,7 +543,10 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
       unsigned char* planes = xdig + buf * I8_XBUF_BYTES;
       const double* xs = stage + buf * I8_TILE * I8_N;
       if (!(dbg & 2)) {
-        constexpr int RG = (I8_TILE / I8_SLICE_WARPS) < 8 ? (I8_TILE / I8_SLICE_WARPS) : 8;  // rows in flight: independent load -> max -> split chains
+        // rows in flight (independent load -> max -> split chains); fewer when the
+        // 16-epilogue-warp layout caps registers near 88 per thread
+        constexpr int RG_MAX = I8_THREADS > 512 ? 4 : 8;
+        constexpr int RG = (I8_TILE / I8_SLICE_WARPS) < RG_MAX ? (I8_TILE / I8_SLICE_WARPS) : RG_MAX;
 #pragma unroll 1
         for (int rb = 0; rb < I8_TILE / I8_SLICE_WARPS; rb += RG) {
           double xv[RG][4];
