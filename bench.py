@@ -296,9 +296,18 @@ def run_ours(args):
     if tensor_core:
         # int8-digit tcgen05 kernel: the FP64 product is exact integer work on
         # the tensor cores; the kernel is bounded by streaming X in and X^A out
-        roofline = {"bound": "hbm", "kernel": "anomaly_i8_kernel (X^A = X + X C, tcgen05.mma kind::i8 on exact byte digits, TMA-staged)",
+        traffic, traffic_src = None, None
+        try:  # DRAM bytes per row from the committed ncu --set full capture, times this launch's rows
+            cap = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                              "r01_anomaly_dram.json")))
+            traffic = cap["dram_bytes_per_row"] * ns_loc
+            traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per row from " + cap["capture"] +
+                           f", x {ns_loc} rows per launch ({cap['ratio_to_algorithmic']:.4f} x algorithmic)")
+        except (OSError, KeyError, ValueError):
+            pass
+        roofline = {"bound": "hbm", "kernel": "anomaly_i8_kernel (X^A = X T, tcgen05.mma kind::i8 on exact byte digits, TMA-staged)",
                     "achieved": anom_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": anom_gbs / hbm_peak,
-                    "traffic": None,
+                    "traffic": traffic, "traffic_source": traffic_src,
                     "algorithmic": f"read X + write X^A = 2*n_state*n_ens*8 = {bytes_anom:.3e} B per launch",
                     "peak_source": peak_src,
                     "fp64_view": {"equivalent_tflops": anom_tflops, "fp64_dmma_peak": FP64_DMMA_PEAK_TFLOPS,
