@@ -568,6 +568,31 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
           }
 #pragma unroll
           for (int u = 0; u < RG; ++u) m[u] = __reduce_max_sync(0xffffffffu, m[u]);  // one REDUX per row
+          // Tiny rows (max|x| < 2^-977, including subnormals) would need a scale above
+          // the fp64 range: rescale them exactly by 2^600 first (warp-uniform, rare), and
+          // take the 600 back out of their exponent shift k.
+          int tsh[RG];
+          bool anytiny = false;
+#pragma unroll
+          for (int u = 0; u < RG; ++u) {
+            tsh[u] = 0;
+            anytiny |= (m[u] != 0u) & ((m[u] >> 20) < 46u);
+          }
+          if (anytiny) {
+#pragma unroll
+            for (int u = 0; u < RG; ++u) {
+              if ((m[u] != 0u) & ((m[u] >> 20) < 46u)) {
+                uint32_t mm = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                  xv[u][b] *= 0x1p600;
+                  mm = max(mm, (uint32_t)__double2hiint(xv[u][b]) & 0x7fffffffu);
+                }
+                m[u] = __reduce_max_sync(0xffffffffu, mm);
+                tsh[u] = 600;
+              }
+            }
+          }
 #pragma unroll
           for (int u = 0; u < RG; ++u) {
             const int r = (I8_TILE / I8_SLICE_WARPS) * sw + rb + u;
@@ -575,8 +600,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
             // Branch-free (so the RG rows interleave): with the biased exponent
             // clamped to bc, scale = 2^(47-e) and rs = 2^(e-30), e = bc - 1022.
             //  * zero row: any finite scale (the digits are 0 and X^A = X exactly);
-            //  * tiny row (max|x| < 2^-977): clamped at bc = 46, the row keeps
-            //    47 - (46 - bexp) bits instead of overflowing the scale;
+            //  * tiny rows were rescaled by 2^600 above (bexp >= 46 now);
             //  * non-finite row: the digits are don't-care and rs = NaN makes the
             //    row NaN, what x T gives in fp64.
             const bool finite_row = bexp != 0x7ff;
@@ -613,7 +637,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
             two_planes(vlo[0], vlo[1], vlo[2], vlo[3], 1u, 0u, w[4], w[5]);  // bytes 1, 0
 #pragma unroll
             for (int p = 0; p < I8_ND; ++p) *reinterpret_cast<uint32_t*>(planes + p * I8_PLANE_BYTES + off) = w[p];
-            const int kv = finite_row ? bc + kbias : INT_MIN;
+            const int kv = finite_row ? bc + kbias - tsh[u] : INT_MIN;
             wslow |= (kv < -1022) | (kv > 961);  // outside the exponent-field fast path
             if (lane == 0) rinfo[(int)(it % (2 * I8_NBUF)) * I8_TILE + r] = kv;
           }

@@ -451,3 +451,40 @@ def test_int8_gram_matches_fp64_gram(heavy):
     assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
     tol = 0.0 if heavy else 1e-13
     assert np.abs(a - b).max() <= tol * np.abs(a).max()
+
+
+def test_tensor_core_anomaly_extreme_rows():
+    """Rows far from unit scale go through the same exact-digit path: tiny rows
+    (max|x| < 2^-977: rescaled by 2^600 before slicing), huge rows (|x| ~ 1e300, the
+    exponent-field slow path), all-zero rows and ordinary rows, one launch; each
+    row against an fp64 X T computed on the host, relative to that row's scale.
+    (Rows entirely in the subnormal range keep only the few bits fp64 has there.)"""
+    import torch
+    dev = torch.device("cuda", 0)
+    n, ns = 128, 4096
+    g = np.random.Generator(np.random.Philox(17))
+    x = g.standard_normal((ns, n))
+    scales = np.ones(ns)
+    scales[0:64] = 2.0 ** -1000    # tiny
+    scales[64:128] = 1e300         # huge (|X T| stays finite: T ~ I)
+    scales[128:192] = 2.0 ** -990   # tiny, another binade
+    x *= scales[:, None]
+    x[192:256] = 0.0               # zero rows
+    t = np.eye(n) + 0.02 * g.standard_normal((n, n))
+    plan = _native.Plan(ns, 1, n, 0)
+    xd = torch.from_numpy(x).to(dev)
+    td = torch.from_numpy(t).to(dev)
+    out = torch.empty_like(xd)
+    s = torch.cuda.current_stream().cuda_stream
+    assert _native.lib().enkf_anomaly_update_f64(plan.handle, xd.data_ptr(), td.data_ptr(), out.data_ptr(), ns, s) == 0
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    # reference in scaled arithmetic (x / scale) T, so the host product itself neither
+    # underflows nor overflows
+    safe = np.where(scales > 0, scales, 1.0)
+    want = ((x / safe[:, None]) @ t) * safe[:, None]
+    assert np.array_equal(got[192:256], np.zeros((64, n)))
+    for lo, hi, tol in ((0, 64, 1e-12), (64, 128, 1e-12), (128, 192, 1e-12), (256, ns, 1e-12)):
+        rowscale = np.abs(want[lo:hi]).max(axis=1, keepdims=True)
+        assert np.all(np.isfinite(got[lo:hi]))
+        assert (np.abs(got[lo:hi] - want[lo:hi]) / rowscale).max() <= tol, (lo, hi)
