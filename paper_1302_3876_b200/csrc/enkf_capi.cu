@@ -123,7 +123,7 @@ cudaError_t launch_gram_ws_t(const enkf_plan* p, const double* X, const double* 
     auto kern = gram128_kernel<ANALYSIS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, W_THREADS, smem, s>>>(
+    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, 32 * (G128_MMA_WARPS + 4), smem, s>>>(
         X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv, p->g128_rows_vv, p->g128_rows_vd,
         p->partial, p->dstatus, nullptr);
     return cudaGetLastError();
@@ -212,7 +212,7 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     auto kern = gram128_kernel<true>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem)) != cudaSuccess)
       return e;
-    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, W_THREADS, gsmem, s>>>(X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv,
+    kern<<<p->g128_cpb_vv + p->g128_cpb_vd, 32 * (G128_MMA_WARPS + 4), gsmem, s>>>(X, Y, idx, r, p->n_state, p->n_obs, ld, p->g128_cpb_vv,
                                                                    p->g128_rows_vv, p->g128_rows_vd, p->partial,
                                                                    p->dstatus, overflow);
     gram128_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->partial, p->g128_cpb_vv, p->g128_cpb_vd, svv,

@@ -664,6 +664,12 @@ gram_ws_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 // 6 stages deep.  Rationale: transform-side DADDs share the FP64 pipe with
 // DMMA, so their count and dependency depth bound the whole pass.
 constexpr int P_STAGES = 6;
+// gram128 DMMA warps: 8 (64x32 warp tiles) or 16 (32x32 tiles: more warps to hide the
+// fragment-load latency, and the V'V block skips 6 of 16 tiles below the diagonal)
+#ifndef G128_MW
+#define G128_MW 8
+#endif
+constexpr int G128_MMA_WARPS = G128_MW;
 constexpr int P_XFORM = 4;  // gram128: transform warps 8..11 (warp 8 also loads)
 __host__ __device__ inline size_t gram128_smem_bytes(int ld) {
   return (size_t)P_STAGES * 2 * W_RT * ld * sizeof(double)
@@ -675,7 +681,7 @@ __host__ __device__ inline size_t gram128_smem_bytes(int ld) {
 // warp tiles (25 % less DMMA work), and get proportionally more rows each
 // (cpb_vv CTAs for V'V, cpb_vd for V'D, chosen by the host to balance).
 template <bool ANALYSIS>
-__global__ void __launch_bounds__(W_THREADS, 1)
+__global__ void __launch_bounds__(32 * (G128_MW + 4), 1)
 gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                const int64_t* __restrict__ idx, const double* __restrict__ r,
                int64_t n_state, int64_t n_obs, int ld, int cpb_vv, int64_t rows_vv,
@@ -709,18 +715,18 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     for (int i = 0; i < P_STAGES; ++i) {
       mbar_init(&load_full[i], 1);
       mbar_init(&op_full[i], 32 * P_XFORM);
-      mbar_init(&op_empty[i], 32 * W_MMA_WARPS);
+      mbar_init(&op_empty[i], 32 * G128_MMA_WARPS);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp >= W_MMA_WARPS) {
+  if (warp >= G128_MMA_WARPS) {
     // ------------------------------------------------- transforms (+ loader)
     // Warps 8..11 transform rows tw, tw+4, tw+8, tw+12 of each stage; warp 8
     // also streams the rows in (idx/r prefetched one stage ahead, one bulk TMA
     // copy per gathered X row and per Y row), S-1 stages ahead of the DMMA warps.
-    const int tw = warp - W_MMA_WARPS;
+    const int tw = warp - G128_MMA_WARPS;
     const double inv_n = 1.0 / 128.0;
     int flags = 0;
     // loader state (warp 8 only)
@@ -861,15 +867,18 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   }
 
 // ------------------------------------------------------------------ DMMA
-  const int wm = warp & 1, wn = warp >> 1;
-  // V'V: rows 64-127 x cols 0-63 lie strictly below the diagonal
-  const bool active = dblk || !(wm == 1 && wn < 2);
-  double acc[8][4][2];
+  constexpr int TM = G128_MMA_WARPS == 16 ? 32 : 64;  // warp tile rows (cols are 32)
+  constexpr int MT = TM / 8;
+  constexpr int WMN = 128 / TM;                        // warp tiles per column
+  const int wm = warp % WMN, wn = warp / WMN;
+  // V'V is symmetric: tiles strictly below the diagonal are not computed
+  const bool active = dblk || (TM * wm < 32 * wn + 32);
+  double acc[MT][4][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int arow = lane & 3, acol = 64 * wm + (lane >> 2), bcol = 32 * wn + (lane >> 2);
+  const int arow = lane & 3, acol = TM * wm + (lane >> 2), bcol = 32 * wn + (lane >> 2);
   for (int t = 0; t < nstages; ++t) {
     const int slot = t % P_STAGES;
     mbar_wait(&op_full[slot], (t / P_STAGES) & 1);
@@ -879,13 +888,13 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     for (int ks = 0; ks < (active ? W_RT / 4 : 0); ++ks) {
       const int row = 4 * ks + arow;
       const double ri = rinv_s[slot * W_RT + row];
-      double a[8], b[4];
+      double a[MT], b[4];
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) a[mt] = as[row * ld + acol + 8 * mt];
+      for (int mt = 0; mt < MT; ++mt) a[mt] = as[row * ld + acol + 8 * mt];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt) b[nt] = bsm[row * ld + bcol + 8 * nt] * ri;
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
     }
@@ -893,8 +902,8 @@ gram128_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   }
   double* out = partial + (size_t)blockIdx.x * W_TILE * W_TILE;
 #pragma unroll
-  for (int mt = 0; mt < 8; ++mt) {
-    const int i = 64 * wm + 8 * mt + (lane >> 2);
+  for (int mt = 0; mt < MT; ++mt) {
+    const int i = TM * wm + 8 * mt + (lane >> 2);
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int j = 32 * wn + 8 * nt + 2 * (lane & 3);
