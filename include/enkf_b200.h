@@ -21,7 +21,8 @@
  *   enkf_analysis_localized_cyclic_f64 enkf.py:193-199 with delta = influence_matrix_cyclic
  *                           (enkf.py:138-164) evaluated on the fly (matrix-free)
  *   enkf_forecast_l96_f64   models/lorenz96.py:31-78  Lorenz96.advance (RK4 steps), bit-exact
- *   enkf_cycle_l96_f64      experiment.py:457-479     forecast -> analysis cycles, device-resident
+ *   enkf_cycle_l96_f64      experiment.py:457-479     forecast -> (inflation) -> analysis cycles, device-resident
+ *   enkf_inflate_f64        enkf.py:123-135           inflate (covariance inflation about the row mean)
  *
  * Layouts (all fp64 row-major, the reference's C-order arrays):
  *   X, XA : [n_state][n_ens]      Y, D, V, Z : [n_obs][n_ens]
@@ -134,12 +135,16 @@ int32_t enkf_forecast_l96_f64(enkf_plan* plan, const double* X, double* Xout, do
  *   for c in [0, n_cycles): X <- forecast(X, steps_per_cycle); X <- analysis(X, Ys[c], idx, r)
  * X is updated in place.  Ys: [n_cycles][n_obs][n_ens].  mean_f / mean_a
  * (optional, [n_cycles][n_state]) receive the forecast / analysis ensemble
- * means.  No host round trip between cycles; the first failing cycle (0-based)
+ * means.  inflation > 1 inflates the forecast (after mean_f) as experiment.py:466-467.  No host round trip between cycles; the first failing cycle (0-based)
  * is returned in *failed_cycle (-1 if none) with its error in status. */
 int32_t enkf_cycle_l96_f64(enkf_plan* plan, double* X, const double* Ys, const int64_t* idx, const double* r,
-                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing,
+                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing, double inflation,
                            double* mean_f, double* mean_a, void* stream, enkf_status* status,
                            int32_t* failed_cycle);
+/* Covariance inflation (enkf.py:123-135): Xout = mean + alpha (X - mean) per row of the
+ * [n_rows][n_ens] ensemble (X may alias Xout); alpha < 1 -> INVALID_ARGUMENT, alpha == 1 copies. */
+int32_t enkf_inflate_f64(const double* X, double* Xout, int64_t n_rows, int64_t n_ens, double alpha,
+                         void* stream);
 
 /* --- staged form (multi-GPU: partial Gram -> allreduce by the caller -> levels) --- */
 

@@ -23,6 +23,7 @@ from .enkf_oracle import (  # noqa: F401
     analysis_step_localized,
     apply_selection,
     cycle_l96,
+    inflate,
     influence_matrix_cyclic,
     innovations,
     l96_advance,

@@ -260,15 +260,28 @@ def l96_advance(x, nsteps, dt=0.05, forcing=8.0):
     return x
 
 
-def cycle_l96(x0, ys, indices, r, steps_per_cycle, dt=0.05, forcing=8.0):
+def inflate(x, alpha):
+    """enkf.py:123-135."""
+    if alpha < 1.0:
+        raise ValueError(f"inflation factor must be >= 1, got {alpha}")
+    x = np.asarray(x, dtype=float)
+    if alpha == 1.0:
+        return x
+    mean = x.mean(axis=1, keepdims=True)
+    return mean + alpha * (x - mean)
+
+
+def cycle_l96(x0, ys, indices, r, steps_per_cycle, dt=0.05, forcing=8.0, inflation=1.0):
     """experiment.py:457-479 closed loop with the lorenz96 model: forecast
-    (enkf.py:202-212) then analysis_step, per cycle; returns the final
-    ensemble and the forecast / analysis ensemble means per cycle."""
+    (enkf.py:202-212), inflation when > 1 (:466-467), then analysis_step, per
+    cycle; returns the final ensemble and the forecast / analysis ensemble means."""
     x = np.asarray(x0, dtype=float)
     mean_f, mean_a = [], []
     for y in ys:
         x = l96_advance(x, steps_per_cycle, dt, forcing)
         mean_f.append(x.mean(axis=1))
+        if inflation > 1.0:
+            x = inflate(x, inflation)
         x = analysis_step(x, y, indices, r)
         mean_a.append(x.mean(axis=1))
     return x, np.stack(mean_f), np.stack(mean_a)

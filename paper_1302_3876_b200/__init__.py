@@ -15,6 +15,7 @@ from .enkf import (
     ObservationBatch,
     SelectionOperator,
     analysis_step,
+    inflate,
     influence_matrix_cyclic,
     innovations,
     member_deviations,
@@ -59,6 +60,7 @@ __all__ = [
     "analysis_step",
     "cycle_l96",
     "forecast_step",
+    "inflate",
     "influence_matrix_cyclic",
     "innovations",
     "level_blocks",

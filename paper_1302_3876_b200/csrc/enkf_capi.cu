@@ -901,8 +901,22 @@ int32_t enkf_forecast_l96_f64(enkf_plan* p, const double* X, double* Xout, doubl
   return enkf_plan_sync_status(p, stream, st);
 }
 
+int32_t enkf_inflate_f64(const double* X, double* Xout, int64_t n_rows, int64_t n_ens, double alpha,
+                         void* stream) {
+  if (!(alpha >= 1.0) || n_ens < 1 || n_rows < 0) return ENKF_INVALID_ARGUMENT;
+  if (n_rows == 0) return ENKF_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (alpha == 1.0) {  // the reference returns x itself
+    if (X == Xout) return ENKF_OK;
+    return cudaMemcpyAsync(Xout, X, sizeof(double) * (size_t)n_rows * n_ens, cudaMemcpyDeviceToDevice, s) == cudaSuccess
+               ? ENKF_OK : ENKF_CUDA_ERROR;
+  }
+  inflate_kernel<<<(unsigned)((n_rows * 32 + 255) / 256), 256, 0, s>>>(X, Xout, n_rows, (int)n_ens, alpha);
+  return cudaGetLastError() == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
+}
+
 int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, const double* r,
-                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing,
+                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing, double inflation,
                            double* mean_f, double* mean_a, void* stream, enkf_status* st,
                            int32_t* failed_cycle) {
   if (failed_cycle) *failed_cycle = -1;
@@ -912,6 +926,10 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
     return ENKF_INVALID_ARGUMENT;
   }
   if (int rc = check_l96(p, dt, steps_per_cycle, st)) return rc;
+  if (!(inflation >= 1.0)) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "inflation factor must be >= 1, got %g", inflation);
+    return ENKF_INVALID_ARGUMENT;
+  }
   if (n_cycles < 0) {
     set_status(st, ENKF_INVALID_ARGUMENT, "negative cycle count");
     return ENKF_INVALID_ARGUMENT;
@@ -939,6 +957,10 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
     e = launch_l96(p, X, X, dt, forcing, steps_per_cycle, s);
     if (e == cudaSuccess && mean_f) {
       row_mean_kernel<<<mean_grid, 256, 0, s>>>(X, mean_f + (size_t)c * p->n_state, p->n_state, p->n);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && inflation > 1.0) {  // experiment.py:466-467, after the forecast error
+      inflate_kernel<<<mean_grid, 256, 0, s>>>(X, X, p->n_state, p->n, inflation);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = launch_gram(p, true, X, Ys + (size_t)c * yelems, idx, r, p->gram, s);

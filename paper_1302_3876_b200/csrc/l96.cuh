@@ -131,6 +131,20 @@ __global__ void l96_stage_kernel(const double* __restrict__ x, const double* __r
   }
 }
 
+// Covariance inflation (enkf.py:123-135): mean + alpha (x - mean) per row, the
+// reference's operation order (no FMA contraction).  Warp per row; X may alias Xout.
+__global__ void inflate_kernel(const double* __restrict__ X, double* __restrict__ Xout, int64_t ns, int n,
+                               double alpha) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= ns) return;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s += X[row * n + c];
+  const double mean = __ddiv_rn(warp_sum(s), (double)n);
+  for (int c = lane; c < n; c += 32)
+    Xout[row * n + c] = __dadd_rn(mean, __dmul_rn(alpha, __dsub_rn(X[row * n + c], mean)));
+}
+
 // Row means of the ensemble (diagnostics of the cycled driver: the forecast
 // and analysis ensemble means the reference's cycle_error uses).  Warp per row.
 __global__ void row_mean_kernel(const double* __restrict__ X, double* __restrict__ out, int64_t ns, int n) {

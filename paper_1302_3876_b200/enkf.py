@@ -142,6 +142,28 @@ def member_deviations(x):
     return out if dev_in else out.cpu().numpy()
 
 
+def inflate(x, alpha: float):
+    """Scale deviations about the ensemble mean by alpha >= 1 on the GPU
+    (enkf.py:123-135; alpha == 1 returns the input as a float array)."""
+    if alpha < 1.0:
+        raise ValueError(f"inflation factor must be >= 1, got {alpha}")
+    dev_in = _is_cuda_tensor(x)
+    if not dev_in:
+        x = np.asarray(x, dtype=float)
+    if alpha == 1.0:
+        return x
+    if x.ndim != 2:
+        raise ValueError("inflate expects an (nstate, nens) ensemble")
+    device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
+    xd = _f64_contig_device(x, device)
+    out = torch.empty_like(xd)
+    _native.lib().enkf_set_device(device.index)
+    code = _native.lib().enkf_inflate_f64(xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1], float(alpha),
+                                          _stream_ptr(device))
+    _native.raise_for_status(code, None, "enkf_inflate_f64")
+    return out if dev_in else out.cpu().numpy()
+
+
 def innovations(obs: ObservationBatch, h: SelectionOperator, x):
     """D = Y - H(X) on the GPU (enkf.py:114-120)."""
     dev_in = _is_cuda_tensor(x)

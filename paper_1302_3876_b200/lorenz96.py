@@ -108,15 +108,19 @@ class CycleResult:
     mean_a: object   # (cycles, nstate) CUDA tensor
 
 
-def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per_cycle: int) -> CycleResult:
+def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per_cycle: int,
+              inflation: float = 1.0) -> CycleResult:
     """Closed-loop cycling on the device: for every cycle c, X <- forecast(X,
-    steps_per_cycle RK4 steps); X <- analysis_step(X, perturbed[c], h, r).
+    steps_per_cycle RK4 steps); X <- inflate(X, inflation) when inflation > 1
+    (experiment.py:466-467); X <- analysis_step(X, perturbed[c], h, r).
 
     ``perturbed``: (cycles, nobs, nens) pre-staged perturbed observations
     (numpy or CUDA tensor).  Failures raise NumericalFailureError naming the
     cycle (1-based, as experiment.py:474-478) chained to the underlying
     SingularUpdateError / DivergenceError / ValueError."""
     cfg = model.config
+    if inflation < 1.0:
+        raise ValueError(f"inflation factor must be >= 1, got {inflation}")
     dev_in = _is_cuda_tensor(x0)
     device = torch.device("cuda", _cuda_ready(x0.device.index if dev_in else None))
     x = _f64_contig_device(x0, device).clone()
@@ -146,7 +150,7 @@ def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per
     with plan.lock:
         code = _native.lib().enkf_cycle_l96_f64(
             plan.handle, x.data_ptr(), ys.data_ptr(), 0 if idx is None else idx.data_ptr(), rd.data_ptr(),
-            cycles, int(steps_per_cycle), cfg.dt, cfg.forcing, mean_f.data_ptr(), mean_a.data_ptr(),
+            cycles, int(steps_per_cycle), cfg.dt, cfg.forcing, float(inflation), mean_f.data_ptr(), mean_a.data_ptr(),
             _stream_ptr(device), ctypes.byref(st), ctypes.byref(failed))
     if code != _native.ENKF_OK:
         try:

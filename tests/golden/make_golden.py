@@ -251,6 +251,24 @@ def lorenz96():
         ys.append(ob.perturbed)
     out["cyc_r"], out["cyc_ys"] = r, np.stack(ys)
     out["cyc_mean_f"], out["cyc_mean_a"], out["cyc_xa"] = np.stack(mf), np.stack(ma), x
+    # inflate (enkf.py:123-135) on seeded ensembles, and the same loop with inflation 1.05
+    # (experiment.py:466-467: after the forecast error, before the analysis)
+    from enkfkit.enkf import inflate
+    for i, (ns_, ne_, a_) in enumerate([(40, 20, 1.05), (256, 16, 1.3), (7, 3, 2.0)]):
+        xi = 8.0 + make_rng(0xB100 + i).standard_normal((ns_, ne_))
+        out[f"inf{i}_meta"] = np.array([0xB100 + i, ns_, ne_])
+        out[f"inf{i}_alpha"] = np.array(a_)
+        out[f"inf{i}_out"] = inflate(xi, a_)
+    x = out["cyc_x0"].copy()
+    mf, ma = [], []
+    for c in range(cycles):
+        x = forecast_step(model, x, c * 0.25, (c + 1) * 0.25)
+        mf.append(x.mean(axis=1))
+        x = inflate(x, 1.05)
+        ob = ref_enkf.ObservationBatch(y=None, perturbed=out["cyc_ys"][c], perturbations=None)
+        x = ref_enkf.analysis_step(x, ob, h, r, "sherman")
+        ma.append(x.mean(axis=1))
+    out["cycinf_mean_f"], out["cycinf_mean_a"], out["cycinf_xa"] = np.stack(mf), np.stack(ma), x
     return out
 
 

@@ -31,7 +31,8 @@ def test_header_declares_the_surface():
     for must in ("enkf_analysis_f64", "enkf_analysis_host_f64", "enkf_ism_solve_f64",
                  "enkf_ism_gram_f64", "enkf_ism_levels_f64", "enkf_anomaly_update_f64",
                  "enkf_plan_create", "enkf_plan_destroy", "enkf_analysis_localized_f64",
-                 "enkf_analysis_localized_cyclic_f64", "enkf_forecast_l96_f64", "enkf_cycle_l96_f64"):
+                 "enkf_analysis_localized_cyclic_f64", "enkf_forecast_l96_f64", "enkf_cycle_l96_f64",
+                 "enkf_inflate_f64"):
         assert must in names
 
 

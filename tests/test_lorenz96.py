@@ -46,6 +46,25 @@ def test_oracle_closed_loop_matches_reference():
     assert rel_err(x, g["cyc_xa"]) <= 1e-12
 
 
+def _inf_cases():
+    g = load("lorenz96")
+    i = 0
+    while f"inf{i}_meta" in g:
+        seed, ns, ne = (int(t) for t in g[f"inf{i}_meta"])
+        yield 8.0 + make_rng(seed).standard_normal((ns, ne)), float(g[f"inf{i}_alpha"]), g[f"inf{i}_out"]
+        i += 1
+
+
+def test_oracle_inflate_and_inflated_loop_match_reference():
+    for x, a, want in _inf_cases():
+        assert np.array_equal(oracle.inflate(x, a), want)
+    g = load("lorenz96")
+    x, mf, ma = oracle.cycle_l96(g["cyc_x0"], g["cyc_ys"], None, g["cyc_r"], 5, inflation=1.05)
+    assert rel_err(ma, g["cycinf_mean_a"]) <= 1e-12 and rel_err(x, g["cycinf_xa"]) <= 1e-12
+    with pytest.raises(ValueError):
+        oracle.inflate(x, 0.9)
+
+
 def test_model_argument_errors():
     with pytest.raises(ValueError):
         L.Lorenz96Config(nstate=3)
@@ -102,6 +121,25 @@ def test_gpu_closed_loop_matches_reference():
     assert rel_err(res.mean_f.cpu().numpy(), g["cyc_mean_f"]) <= 1e-9
     assert rel_err(res.mean_a.cpu().numpy(), g["cyc_mean_a"]) <= 1e-9
     assert rel_err(res.x.cpu().numpy(), g["cyc_xa"]) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_gpu_inflate_and_inflated_loop():
+    for x, a, want in _inf_cases():
+        got = P.inflate(x, a)
+        assert rel_err(got, want) <= 1e-15
+        assert np.abs(got.mean(axis=1) - x.mean(axis=1)).max() <= 1e-13 * np.abs(x).max()
+    x = np.ones((8, 3))
+    assert P.inflate(x, 1.0) is x
+    with pytest.raises(ValueError):
+        P.inflate(x, 0.5)
+    g = load("lorenz96")
+    model = P.Lorenz96(P.Lorenz96Config(nstate=g["cyc_x0"].shape[0]))
+    res = P.cycle_l96(model, g["cyc_x0"], g["cyc_ys"], P.SelectionOperator.identity(), g["cyc_r"], 5,
+                      inflation=1.05)
+    assert rel_err(res.mean_f.cpu().numpy(), g["cycinf_mean_f"]) <= 1e-9
+    assert rel_err(res.mean_a.cpu().numpy(), g["cycinf_mean_a"]) <= 1e-9
+    assert rel_err(res.x.cpu().numpy(), g["cycinf_xa"]) <= 1e-9
 
 
 @pytest.mark.gpu
