@@ -270,7 +270,11 @@ def run_ours(args):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
             el = float(et.item())
         e2e = {"value": args.e2e_steps / el, "unit": "steps/s",
-               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes + idx_loc.nbytes) * world,
+               # world 1, pinned X: the observed rows X[idx] cross PCIe twice (the
+               # gather that feeds the Gram pass, then with their X chunk)
+               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes + idx_loc.nbytes
+                                         + (y_h.numel() * 8 if world == 1 and os.environ.get("ENKF_HOST_STREAM", "1") != "0"
+                                            else 0)) * world,
                "d2h_bytes_per_step": int(x_h.numel() * 8) * world, "steps": args.e2e_steps,
                "api": ("paper_1302_3876_b200.analysis_step(numpy host arrays) -> enkf_analysis_host_f64" if world == 1
                        else "paper_1302_3876_b200.distributed.ShardedAnalysis.step from pinned host shards")}

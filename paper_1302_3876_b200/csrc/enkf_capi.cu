@@ -1,6 +1,7 @@
 // enkf_capi.cu — the C ABI (include/enkf_b200.h) over the sm_100a kernels.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
@@ -16,6 +17,7 @@
 #include "localized.cuh"
 #include "l96.cuh"
 #include "gram_i8.cuh"
+#include "host_stream.cuh"
 
 using namespace enkf;
 
@@ -31,6 +33,9 @@ struct enkf_plan {
   bool anomaly_i8 = true;      // tensor-core (int8 digit) anomaly update, N == 128
   int i8_dbg = 0;              // profiling-only role skips (ENKF_I8_DBG)
   bool levels_blocked = true;  // blocked (LB levels per barrier) Sherman-Morrison recursion
+  bool host_streamed = true;   // pipelined host path for pinned X / XA (ENKF_HOST_STREAM=0 disables)
+  size_t host_chunk_bytes = (size_t)256 << 20;
+  bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
   bool gram_i8 = false;        // tensor-core (int8 digit) Gram, N == 128 analysis mode (opt-in: ENKF_GRAM=i8)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   int64_t g8_rows = 0;         // observation rows per group (multiple of 64)
@@ -54,6 +59,12 @@ struct enkf_plan {
   double* hr = nullptr;
   int64_t* hidx = nullptr;
   cudaStream_t hstream = nullptr;
+  // streamed host path (pinned X and XA): compact observed rows, copy streams,
+  // one event per X chunk
+  double* hxo = nullptr;
+  cudaStream_t hs_in = nullptr, hs_out = nullptr;
+  cudaEvent_t ev_obs = nullptr, ev_anom = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
   // pinned staging ring for pageable host buffers
   char* ring[2] = {nullptr, nullptr};
   cudaEvent_t ring_ev[2] = {nullptr, nullptr};
@@ -544,6 +555,9 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
   if (const char* env = getenv("ENKF_GRAM")) p->gram_i8 = (strcmp(env, "i8") == 0);
+  if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
+  if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
+  if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
   {
     int64_t rr = (n_obs + p->g8_groups - 1) / p->g8_groups;
@@ -609,6 +623,12 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->hr);
   cudaFree(p->hidx);
   if (p->hstream) cudaStreamDestroy(p->hstream);
+  cudaFree(p->hxo);
+  if (p->hs_in) cudaStreamDestroy(p->hs_in);
+  if (p->hs_out) cudaStreamDestroy(p->hs_out);
+  if (p->ev_obs) cudaEventDestroy(p->ev_obs);
+  if (p->ev_anom) cudaEventDestroy(p->ev_anom);
+  for (cudaEvent_t ev : p->chunk_ev) cudaEventDestroy(ev);
   cudaFree(p->locV);
   cudaFree(p->locD);
   cudaFree(p->locZ);
@@ -691,6 +711,129 @@ int32_t enkf_analysis_f64(enkf_plan* p, const double* X, const double* Y, const 
   return enkf_plan_sync_status(p, stream, st);
 }
 
+namespace {
+// Device address of a page-locked, mapped host buffer (cudaHostAlloc'd memory,
+// torch pin_memory, or cudaHostRegister'ed with mapping), or null.
+const void* mapped_device_ptr(const void* h) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+}
+
+// Host-buffer analysis with page-locked X and XA (enkf.py:167-192 on host
+// arrays).  Only the observed rows and Y are needed before T exists, so:
+//   1. r, idx, Y by DMA; X[idx] gathered by SM loads over PCIe (gather_rows_kernel)
+//   2. Gram pass on the compact rows (identity H), levels -> T
+//   3. X by DMA in chunks on a second stream (starts right after step 1's
+//      traffic, overlapping the Gram), the anomaly update of each chunk as it
+//      lands, X^A chunks out by DMA on a third stream: the two PCIe directions
+//      run concurrently.
+// The status is read after step 2 (a failed step returns before any X^A is
+// copied, after the in-flight X DMA has drained).
+int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, const double* Y_h,
+                           const int64_t* idx_h, const double* r_h, double* XA_h, enkf_status* st) {
+  const size_t n = (size_t)p->n;
+  const size_t row_bytes = n * sizeof(double);
+  cudaStream_t s = p->hstream;
+  if (!p->hxo) {
+    CUDA_TRY(cudaMalloc(&p->hxo, row_bytes * (size_t)p->n_obs + 16), st);
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hs_in, cudaStreamNonBlocking), st);
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hs_out, cudaStreamNonBlocking), st);
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_obs, cudaEventDisableTiming), st);
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_anom, cudaEventDisableTiming), st);
+  }
+  int64_t chunk_rows = (int64_t)(p->host_chunk_bytes / row_bytes);
+  if (chunk_rows < 1024) chunk_rows = 1024;
+  const int64_t nchunks = (p->n_state + chunk_rows - 1) / chunk_rows;
+  while ((int64_t)p->chunk_ev.size() < nchunks) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
+    p->chunk_ev.push_back(ev);
+  }
+  cudaEvent_t tr[7] = {};
+  if (p->host_trace)
+    for (auto& ev : tr) cudaEventCreate(&ev);
+  auto mark = [&](int i, cudaStream_t ms) {
+    if (p->host_trace) cudaEventRecord(tr[i], ms);
+  };
+  // 1. observation side
+  mark(0, s);
+  CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
+  CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
+  CUDA_TRY(copy_h2d(p, p->hidx, idx_h, sizeof(int64_t) * (size_t)p->n_obs, s), st);
+  CUDA_TRY(copy_h2d(p, p->hy, Y_h, row_bytes * (size_t)p->n_obs, s), st);
+  mark(1, s);
+  {
+    const int grid = p->num_sms * 8;
+    const bool vec = (n % 2 == 0) && aligned16(Xmap) && aligned16(p->hxo);
+    if (vec)
+      gather_rows_kernel<true><<<grid, GATHER_THREADS, 0, s>>>(Xmap, p->hidx, p->hxo, p->n_obs, p->n_state,
+                                                               (int)n, p->dstatus);
+    else
+      gather_rows_kernel<false><<<grid, GATHER_THREADS, 0, s>>>(Xmap, p->hidx, p->hxo, p->n_obs, p->n_state,
+                                                                (int)n, p->dstatus);
+    CUDA_TRY(cudaGetLastError(), st);
+  }
+  mark(2, s);  // X[idx] gathered
+  CUDA_TRY(cudaEventRecord(p->ev_obs, s), st);
+  // 3a. the X stream starts once the observation traffic is through
+  CUDA_TRY(cudaStreamWaitEvent(p->hs_in, p->ev_obs, 0), st);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r0 = c * chunk_rows;
+    const int64_t rows = std::min<int64_t>(chunk_rows, p->n_state - r0);
+    CUDA_TRY(cudaMemcpyAsync(p->hx + (size_t)r0 * n, X_h + (size_t)r0 * n, (size_t)rows * row_bytes,
+                             cudaMemcpyHostToDevice, p->hs_in), st);
+    CUDA_TRY(cudaEventRecord(p->chunk_ev[c], p->hs_in), st);
+  }
+  // 2. Gram on the compact observed rows, levels
+  {
+    CUDA_TRY(launch_gram(p, true, p->hxo, p->hy, nullptr, p->hr, p->gram, s), st);
+    const double cscale = 1.0 / std::sqrt((double)(p->n - 1));
+    CUDA_TRY(launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s), st);
+  }
+  mark(3, s);  // T ready
+  {
+    int rc = enkf_plan_sync_status(p, s, st);
+    if (rc != ENKF_OK) {
+      cudaStreamSynchronize(p->hs_in);  // the caller's X must not be read after return
+      return rc;
+    }
+  }
+  // 3b. anomaly update chunk by chunk (in place), X^A out
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r0 = c * chunk_rows;
+    const int64_t rows = std::min<int64_t>(chunk_rows, p->n_state - r0);
+    double* dx = p->hx + (size_t)r0 * n;
+    CUDA_TRY(cudaStreamWaitEvent(s, p->chunk_ev[c], 0), st);
+    CUDA_TRY(launch_rowgemm<0>(p, dx, p->T, nullptr, nullptr, dx, rows, s), st);
+    CUDA_TRY(cudaEventRecord(p->ev_anom, s), st);
+    CUDA_TRY(cudaStreamWaitEvent(p->hs_out, p->ev_anom, 0), st);
+    CUDA_TRY(cudaMemcpyAsync(XA_h + (size_t)r0 * n, dx, (size_t)rows * row_bytes, cudaMemcpyDeviceToHost,
+                             p->hs_out), st);
+  }
+  mark(4, p->hs_in);   // all of X in
+  mark(5, s);          // last anomaly chunk
+  mark(6, p->hs_out);  // all of X^A out
+  CUDA_TRY(cudaStreamSynchronize(p->hs_out), st);
+  CUDA_TRY(cudaStreamSynchronize(s), st);
+  if (p->host_trace) {
+    cudaStreamSynchronize(p->hs_in);
+    float t[7] = {};
+    for (int i = 1; i < 7; ++i) cudaEventElapsedTime(&t[i], tr[0], tr[i]);
+    const double ob = (double)(row_bytes * (size_t)p->n_obs);
+    fprintf(stderr,
+            "[enkf host] Y in %.1f ms (%.1f GB/s)  gather %.1f ms (%.1f GB/s)  T ready %.1f  X in %.1f  "
+            "anomaly done %.1f  XA out %.1f ms\n",
+            t[1], ob / (t[1] * 1e6), t[2] - t[1], ob / ((t[2] - t[1]) * 1e6), t[3], t[4], t[5], t[6]);
+    for (auto& ev : tr) cudaEventDestroy(ev);
+  }
+  return ENKF_OK;
+}
+}  // namespace
+
 int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_h,
                                const int64_t* idx_h, const double* r_h, double* XA_h,
                                enkf_status* st) {
@@ -708,6 +851,11 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     CUDA_TRY(cudaMalloc(&p->hidx, sizeof(int64_t) * (size_t)p->n_obs + 16), st);
   }
   cudaStream_t s = p->hstream;
+  if (idx_h && p->n_obs > 0 && p->host_streamed) {
+    const void* Xmap = mapped_device_ptr(X_h);
+    if (Xmap && is_pinned(XA_h))
+      return analysis_host_streamed(p, X_h, (const double*)Xmap, Y_h, idx_h, r_h, XA_h, st);
+  }
   CUDA_TRY(copy_h2d(p, p->hx, X_h, sizeof(double) * (size_t)p->n_state * n, s), st);
   CUDA_TRY(copy_h2d(p, p->hy, Y_h, sizeof(double) * (size_t)p->n_obs * n, s), st);
   CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
