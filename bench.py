@@ -288,6 +288,7 @@ def run_ours(args):
     flop_anom = 2.0 * ns_loc * n * n
     anom_tflops = flop_anom / (t_anom * 1e-3) / 1e12
     flop_gram = 2.0 * nobs_loc * n * (2 * n)
+    gram_i8 = n == 128 and os.environ.get("ENKF_GRAM", "i8") != "fp64"
     bytes_anom = 2.0 * ns_loc * n * 8
     bytes_gram = nobs_loc * (2 * n * 8 + 16)
     try:
@@ -341,11 +342,17 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)},
         "kernels_ms": {"gram": t_gram, "allreduce": t_ar, "levels": t_lev, "anomaly": t_anom},
         "roofline": roofline,
-        "gram_kernel": {"tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None,
-                        "frac_fp64": (flop_gram / (t_gram * 1e-3) / 1e12) / FP64_DMMA_PEAK_TFLOPS if t_gram > 0 else None,
-                        "hbm_gbs": bytes_gram / (t_gram * 1e-3) / 1e9 if t_gram > 0 else None},
+        "gram_kernel": {"impl": ("gram_i8_slice_kernel + gram_i8_mma_kernel (exact byte-digit products on tcgen05 "
+                                 "kind::i8; ENKF_GRAM=fp64 selects the FP64 DMMA gram128_kernel)") if gram_i8 else
+                                "gram128_kernel (FP64 DMMA)",
+                        "fp64_equiv_tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None,
+                        "fp64_equiv_frac_of_dmma_peak": (flop_gram / (t_gram * 1e-3) / 1e12) / FP64_DMMA_PEAK_TFLOPS
+                        if t_gram > 0 else None,
+                        "hbm_gbs_compulsory": bytes_gram / (t_gram * 1e-3) / 1e9 if t_gram > 0 else None},
         "clocks": clocks.summary(),
-        "gpu_launches": 4 * args.steps,
+        # kernels per step: Gram (int8: scales, slice, MMA, reduce + the two flag-gated
+        # FP64-fallback kernels, which exit at once | FP64: gram128 + reduce); levels; anomaly
+        "gpu_launches": ((6 if gram_i8 else 2) + 1 + 1) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }

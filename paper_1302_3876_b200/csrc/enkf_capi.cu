@@ -36,11 +36,10 @@ struct enkf_plan {
   bool host_streamed = true;   // pipelined host path for pinned X / XA (ENKF_HOST_STREAM=0 disables)
   size_t host_chunk_bytes = (size_t)256 << 20;
   bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
-  bool gram_i8 = false;        // tensor-core (int8 digit) Gram, N == 128 analysis mode (opt-in: ENKF_GRAM=i8)
+  bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
-  int64_t g8_rows = 0;         // observation rows per group (multiple of 64)
-  double* g8_rinv = nullptr;   // [n_obs + 64] 1/r
-  unsigned long long* g8_meta = nullptr;  // [384] sampled column maxima, then the overflow flag
+  unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images
+  unsigned long long* g8_meta = nullptr;  // [256] sampled column maxima, then the overflow flag
   double* g8_partial = nullptr;           // [groups][4][128][64]
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
@@ -190,30 +189,43 @@ cudaError_t launch_gram(enkf_plan* p, bool analysis, const double* X, const doub
   return cudaGetLastError();
 }
 
-// int8 tensor-core Gram (gram_i8.cuh): 1/r, sampled column scales, the digit
-// kernel, the reduce, and the FP64 gram128 pass gated on the overflow flag.
+// int8 tensor-core Gram (gram_i8.cuh): sampled column scales, the slice pass
+// (operand images in HBM), the MMA pass, the reduce, and the FP64 gram128 pass
+// gated on the overflow flag.
 cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
                            const double* r, double* gram, cudaStream_t s) {
   const int n = p->n;
   cudaError_t e = cudaSuccess;
-  const int64_t n_pad = p->n_obs + 64;
-  if (!p->g8_rinv) {
-    e = cudaMalloc(&p->g8_rinv, sizeof(double) * (size_t)n_pad);
-    if (e == cudaSuccess) e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (3 * G8_N + 2));
+  const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
+  if (!p->g8_planes) {
+    e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES);
+    if (e == cudaSuccess) e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2));
     if (e == cudaSuccess)
       e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS);
     if (e != cudaSuccess) return e;
   }
-  int* overflow = reinterpret_cast<int*>(p->g8_meta + 3 * G8_N);
-  if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (3 * G8_N + 2), s)) != cudaSuccess) return e;
-  const int rgrid = (int)std::min<int64_t>((n_pad + 255) / 256, (int64_t)p->num_sms * 8);
-  rinv_kernel<<<rgrid, 256, 0, s>>>(r, p->g8_rinv, p->n_obs, n_pad, p->dstatus);
-  gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, p->g8_rinv, p->n_state, p->n_obs, p->g8_meta);
-  const size_t smem = gram_i8_smem_bytes();
-  if ((e = cudaFuncSetAttribute(gram_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-    return e;
-  gram_i8_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(X, Y, idx, p->g8_rinv, p->g8_meta, p->n_state, p->n_obs,
-                                                            p->g8_rows, p->g8_partial, overflow, p->dstatus, 0u);
+  int* overflow = reinterpret_cast<int*>(p->g8_meta + 2 * G8_N);
+  if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (2 * G8_N + 2), s)) != cudaSuccess) return e;
+  gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, r, p->n_state, p->n_obs, p->g8_meta);
+  {
+    const size_t smem = gram_i8_slice_smem_bytes();
+    if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * 3);
+    gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
+                                                                         p->n_obs, n_blocks, p->g8_planes, overflow,
+                                                                         p->dstatus);
+  }
+  {
+    const size_t smem = gram_i8_smem_bytes();
+    if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
+    gram_i8_mma_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
+                                                                  p->g8_partial, overflow);
+  }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
   gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
   // FP64 fallback, a no-op unless an element fell outside the sampled scales
@@ -554,16 +566,11 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
-  if (const char* env = getenv("ENKF_GRAM")) p->gram_i8 = (strcmp(env, "i8") == 0);
+  if (const char* env = getenv("ENKF_GRAM")) p->gram_i8 = (strcmp(env, "fp64") != 0);
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
   if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
-  {
-    int64_t rr = (n_obs + p->g8_groups - 1) / p->g8_groups;
-    rr = (rr + G8_KB - 1) / G8_KB * G8_KB;
-    p->g8_rows = rr < G8_KB ? G8_KB : rr;
-  }
 
   // gram128 split: the V'V CTAs do 3/4 of the DMMA work of the V'D CTAs (and
   // lighter transforms), so they get fewer CTAs with more rows each.
@@ -633,7 +640,7 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->locD);
   cudaFree(p->locZ);
   cudaFree(p->l96ws);
-  cudaFree(p->g8_rinv);
+  cudaFree(p->g8_planes);
   cudaFree(p->g8_meta);
   cudaFree(p->g8_partial);
   cudaFree(p->cyc_status);
@@ -1135,9 +1142,6 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
   return ENKF_OK;
 }
 
-__attribute__((visibility("default"))) int32_t enkf_debug_g8_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, enkf::g_g8_trace, sizeof(enkf::g_g8_trace)) == cudaSuccess ? 0 : 5;
-}
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {

@@ -425,9 +425,19 @@ g = torch.Generator(device=dev); g.manual_seed(11)
 x = torch.randn((ns, 1), dtype=torch.float64, device=dev, generator=g) + (0.5 + 1.5 * torch.rand((ns, 1), dtype=torch.float64, device=dev, generator=g)) * torch.randn((ns, n), dtype=torch.float64, device=dev, generator=g)
 idx = torch.sort(torch.randperm(ns, device=dev, generator=g)[:no]).values
 y = x[idx].mean(dim=1, keepdim=True) + torch.randn((no, n), dtype=torch.float64, device=dev, generator=g)
-if heavy:
+if heavy == 1:
     y[no // 3, 5] = 1e6
+if heavy == 2:
+    # an element whose 48-bit value sits just below 2^47 of its column scale, where
+    # V + bias no longer fits six balanced digits: must take the overflow route
+    e = (0.2 * torch.randn((no, n), dtype=torch.float64, device=dev, generator=g)).clamp(-0.2, 0.2)
+    e[::16, :] = 0.25
+    e[::16, 5] = 1.0
+    e[17, 5] = 7.99
+    y = x[idx] + e
 r = 0.25 + 0.75 * torch.rand((no,), dtype=torch.float64, device=dev, generator=g)
+if heavy == 2:
+    r = torch.ones((no,), dtype=torch.float64, device=dev)
 plan = _native.Plan(ns, no, n, 0)
 gram = torch.empty((n, 2 * n), dtype=torch.float64, device=dev)
 assert lib.enkf_ism_gram_f64(plan.handle, x.data_ptr(), y.data_ptr(), idx.data_ptr(), r.data_ptr(), gram.data_ptr(), s) == 0
@@ -442,10 +452,11 @@ np.save(sys.argv[2], gram.cpu().numpy())
     return np.load(out)
 
 
-@pytest.mark.parametrize("heavy", [False, True])
+@pytest.mark.parametrize("heavy", [0, 1, 2])
 def test_int8_gram_matches_fp64_gram(heavy):
-    """ENKF_GRAM=i8: the exact-digit tcgen05 Gram agrees with the FP64 DMMA Gram to
-    rounding level; a heavy-tailed element outside the sampled scales takes the
+    """The exact-digit tcgen05 Gram (default for N = 128) agrees with the FP64 DMMA
+    Gram (ENKF_GRAM=fp64) to rounding level; a heavy-tailed element outside the
+    sampled scales (1), or one at the top edge of the digit range (2), takes the
     device-gated FP64 fallback (then the two are identical)."""
     a, b = _gram_with("fp64", heavy), _gram_with("i8", heavy)
     assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
