@@ -38,7 +38,10 @@ constexpr int I8_CHUNK = I8_CHUNK_ROWS;  // rows per MMA (N of the instruction)
 // 32-row buffer (N = 32 halves the MMA count; the epilogue drains before reuse)
 constexpr int I8_ABUF = I8_CHUNK == 16 ? 2 : 1;
 constexpr int I8_ND = 6;          // byte digits per value
-constexpr int I8_LMAX = 8;        // keep digit pairs with p + q <= 8
+#ifndef I8_LMAX_DEF
+#define I8_LMAX_DEF 8
+#endif
+constexpr int I8_LMAX = I8_LMAX_DEF;  // keep digit pairs with p + q <= I8_LMAX (8; 7 measured in DESIGN §5)
 constexpr int I8_NLEV = I8_LMAX - 1;  // levels 2..8
 #ifndef I8_SW
 #define I8_SW 4
@@ -454,8 +457,9 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         const bool slow = rflag[(int)(it % (2 * I8_NBUF)) * I8_SLICE_WARPS + (r0 >> 3)] != 0;
         auto sprime = [&](int r) {
           const int d2 = (int)v[0][r], d3 = (int)v[1][r], d4 = (int)v[2][r], d5 = (int)v[3][r];
-          const int d6 = (int)v[4][r], d7 = (int)v[5][r], d8 = (int)v[6][r];
-          const int small = d6 * 16 + ((d7 >> 4) + (d8 >> 12));  // |.| < 2^31
+          const int d6 = (int)v[4][r], d7 = (int)v[5][r];
+          int small = d6 * 16 + (d7 >> 4);  // |.| < 2^31
+          if constexpr (I8_NLEV > 6) small += (int)v[I8_NLEV > 6 ? 6 : 0][r] >> 12;
           long long sp = (long long)d5 * 4096 + (long long)small;
           sp += (long long)d4 * 1048576;
           sp += (long long)d3 * 268435456;
