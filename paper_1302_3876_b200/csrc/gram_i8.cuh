@@ -45,6 +45,11 @@ constexpr int G8_BSL = G8_NS * G8_KB;             // 2 KiB: a 64-member slice of
 constexpr int G8_STAGE = G8_ND * G8_PLANE + G8_ND * G8_BSL;  // 36 KiB: A planes + B slices
 constexpr int G8_NST = 5;        // stage ring depth
 constexpr int G8_THREADS = 6 * 32;  // producer, MMA issuer, 4 flush warps
+#ifndef G8_TS
+#define G8_TS 1                  // A operand (P digit planes) from TMEM (tcgen05.cp), B from smem
+#endif
+constexpr int G8_ATM = G8_NLEV * G8_NS;  // TMEM column of the A planes (after the 7 level accumulators)
+static_assert(G8_ATM + 8 * G8_ND <= 512, "TMEM: accumulators + A planes");
 constexpr int G8_SAMPLE = 16;    // pre-pass samples every 16th observation row
 constexpr int G8_HEADROOM = 2;   // scale exponent headroom (bits) over the sampled max
 constexpr int G8_SLICE_THREADS = 256;
@@ -135,11 +140,117 @@ __global__ void __launch_bounds__(256) gram_i8_scales_kernel(const double* __res
 }
 
 // ---------------------------------------------------------------------------
-// Slice pass.  Phase 1 (warp w: rows 4w..4w+3 of the block, lane: members
-// lane + 32j): the biased 48-bit integers V + 0x808080808080 of P and Q into
-// shared memory [row][256].  Phase 2 (lanes 0-15 / 16-31: 16 members, K-chunk
-// 0 / 1): 16 rows of one member -> 6 planes x 16 bytes, one 16-byte store per
-// plane; a warp writes 16 whole 32-byte plane rows (512 contiguous bytes).
+// Slicing of one 32-row block by 8 warps (256 threads, slicer thread index st).
+// Phase 1 (warp w: rows 4w..4w+3 of the block, lane: members lane + 32j): the
+// biased 48-bit integers V + 0x808080808080 of P and Q into shared memory
+// vals[row][256].  Phase 2 (lanes 0-15 / 16-31: 16 members, K-chunk 0 / 1): 16
+// rows of one member -> 6 planes x 16 bytes, one 16-byte store per plane; a warp
+// writes 16 whole 32-byte plane rows (512 contiguous bytes) of the 48 KiB image
+// `out`.  `sync` is the slicers' barrier (between the phases, and after phase 2
+// so vals can be reused).
+template <class Sync>
+__device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, const double* __restrict__ Y,
+                                               const int64_t* __restrict__ idx, const double* __restrict__ r,
+                                               int64_t n_state, int64_t n_obs, int64_t blk, int st,
+                                               const double (&sp)[4], const double (&sq)[4],
+                                               unsigned long long* vals, unsigned char* __restrict__ out,
+                                               int& flags, int& ovf, Sync sync) {
+  constexpr unsigned long long kBias = 0x808080808080ull;
+  const int lane = st & 31, warp = st >> 5;
+  // ---- phase 1
+  const int64_t g0 = blk * G8_KB + 4 * warp;
+  int64_t src[4];
+  double rv[4];
+  bool valid[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t g = g0 + u;
+    valid[u] = g < n_obs;
+    src[u] = g;
+    rv[u] = 1.0;
+    if (valid[u]) {
+      rv[u] = r[g];
+      if (idx) {
+        src[u] = idx[g];
+        if (lane == 0 && g > 0 && idx[g - 1] >= src[u]) flags |= FLAG_IDX_ORDER;
+        if (src[u] < 0 || src[u] >= n_state) {
+          flags |= FLAG_IDX_RANGE;
+          valid[u] = false;
+        }
+      }
+      if (!isfinite(rv[u])) flags |= FLAG_NONFINITE;
+      else if (!(rv[u] > 0.0)) flags |= FLAG_R_NONPOS;
+    }
+  }
+  double xv[4][4], yv[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      xv[u][j] = valid[u] ? __ldcs(X + src[u] * G8_N + lane + 32 * j) : 0.0;
+      yv[u][j] = valid[u] ? __ldcs(Y + (g0 + u) * G8_N + lane + 32 * j) : 0.0;
+    }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double mean = warp_sum((xv[u][0] + xv[u][1]) + (xv[u][2] + xv[u][3])) * (1.0 / G8_N);
+    const double sr = valid[u] ? g8_sqrt_rho(rv[u]) : 0.0;
+    unsigned long long* vrow = vals + (4 * warp + u) * G8_VLD;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // V = round(v 2^(47-e)): fma(v, sc, 1.5 2^52) holds V in its low 51 bits (the
+      // high word minus 0x43380000 is floor(V / 2^32)).  The six balanced digits
+      // represent V iff V + bias lies in [0, 2^48): anything else (|V| near or
+      // above 2^47, non-finite inputs) sets the overflow flag.
+      const double tp = fma(sr * (xv[u][j] - mean), sp[j], 6755399441055744.0);
+      const double tq = fma(sr * (yv[u][j] - xv[u][j]), sq[j], 6755399441055744.0);
+      const int hp = __double2hiint(tp) - 0x43380000, hq = __double2hiint(tq) - 0x43380000;
+      const unsigned long long bp = ((unsigned long long)(uint32_t)hp << 32 | (uint32_t)__double2loint(tp)) + kBias;
+      const unsigned long long bq = ((unsigned long long)(uint32_t)hq << 32 | (uint32_t)__double2loint(tq)) + kBias;
+      ovf |= ((uint32_t)(bp >> 32) >= 0x10000u) | ((uint32_t)(bq >> 32) >= 0x10000u);
+      vrow[lane + 32 * j] = bp;
+      vrow[G8_N + lane + 32 * j] = bq;
+    }
+  }
+  sync();
+  // ---- phase 2: two passes of 128 (member, chunk) items per warp-half
+#pragma unroll 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int m = 128 * pass + 16 * warp + (lane & 15);  // 0..255: P members, then Q
+    const int ck = lane >> 4;                            // K chunk: rows 16ck..16ck+15
+    uint32_t w[G8_ND][4];
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      uint32_t vlo[4], vhi[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned long long v = vals[(16 * ck + 4 * q4 + u) * G8_VLD + m];
+        vlo[u] = (uint32_t)v;
+        vhi[u] = (uint32_t)(v >> 32);
+      }
+      // plane p (1..6) = byte (6-p) of the biased value, ^ 0x80; 4 rows per word
+      auto two_planes = [&](const uint32_t (&x)[4], uint32_t bi, uint32_t bj, uint32_t& wi, uint32_t& wj) {
+        const uint32_t sel = bi | ((bi + 4u) << 4) | (bj << 8) | ((bj + 4u) << 12);
+        const uint32_t A = __byte_perm(x[0], x[1], sel);
+        const uint32_t B = __byte_perm(x[2], x[3], sel);
+        wi = __byte_perm(A, B, 0x5410) ^ 0x80808080u;
+        wj = __byte_perm(A, B, 0x7632) ^ 0x80808080u;
+      };
+      two_planes(vhi, 1u, 0u, w[0][q4], w[1][q4]);
+      two_planes(vlo, 3u, 2u, w[2][q4], w[3][q4]);
+      two_planes(vlo, 1u, 0u, w[4][q4], w[5][q4]);
+    }
+    const int mm = m & (G8_N - 1);
+    const size_t off = (size_t)(m >= G8_N ? G8_ND * G8_PLANE : 0) + (size_t)mm * 32 +
+                       (size_t)((ck ^ ((mm >> 2) & 1)) << 4);
+#pragma unroll
+    for (int p = 0; p < G8_ND; ++p)
+      *reinterpret_cast<uint4*>(out + off + (size_t)p * G8_PLANE) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+  }
+  sync();
+}
+
+// Slice pass (two-kernel form, ENKF_GRAM=i8split): every 32-row block -> its
+// operand image in HBM.
 __global__ void __launch_bounds__(G8_SLICE_THREADS)
 gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int64_t* __restrict__ idx,
                      const double* __restrict__ r, const unsigned long long* __restrict__ cmax, int64_t n_state,
@@ -148,7 +259,7 @@ gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   extern __shared__ __align__(16) unsigned char g8s_raw[];
   unsigned long long* vals = reinterpret_cast<unsigned long long*>(g8s_raw);  // [32][G8_VLD]
   double* scl = reinterpret_cast<double*>(vals + G8_KB * G8_VLD);              // [256]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   for (int c = tid; c < 2 * G8_N; c += G8_SLICE_THREADS) scl[c] = g8_scale(cmax[c]);
   __syncthreads();
   double sp[4], sq[4];
@@ -157,102 +268,10 @@ gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     sp[j] = scl[lane + 32 * j];
     sq[j] = scl[G8_N + lane + 32 * j];
   }
-  constexpr unsigned long long kBias = 0x808080808080ull;
   int flags = 0, ovf = 0;
-  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x) {
-    // ---- phase 1
-    const int64_t g0 = blk * G8_KB + 4 * warp;
-    int64_t src[4];
-    double rv[4];
-    bool valid[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t g = g0 + u;
-      valid[u] = g < n_obs;
-      src[u] = g;
-      rv[u] = 1.0;
-      if (valid[u]) {
-        rv[u] = r[g];
-        if (idx) {
-          src[u] = idx[g];
-          if (lane == 0 && g > 0 && idx[g - 1] >= src[u]) flags |= FLAG_IDX_ORDER;
-          if (src[u] < 0 || src[u] >= n_state) {
-            flags |= FLAG_IDX_RANGE;
-            valid[u] = false;
-          }
-        }
-        if (!isfinite(rv[u])) flags |= FLAG_NONFINITE;
-        else if (!(rv[u] > 0.0)) flags |= FLAG_R_NONPOS;
-      }
-    }
-    double xv[4][4], yv[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        xv[u][j] = valid[u] ? __ldcs(X + src[u] * G8_N + lane + 32 * j) : 0.0;
-        yv[u][j] = valid[u] ? __ldcs(Y + (g0 + u) * G8_N + lane + 32 * j) : 0.0;
-      }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double mean = warp_sum((xv[u][0] + xv[u][1]) + (xv[u][2] + xv[u][3])) * (1.0 / G8_N);
-      const double sr = valid[u] ? g8_sqrt_rho(rv[u]) : 0.0;
-      unsigned long long* vrow = vals + (4 * warp + u) * G8_VLD;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        // V = round(v 2^(47-e)): fma(v, sc, 1.5 2^52) holds V in its low 51 bits (the
-        // high word minus 0x43380000 is floor(V / 2^32)).  The six balanced digits
-        // represent V iff V + bias lies in [0, 2^48): anything else (|V| near or
-        // above 2^47, non-finite inputs) sets the overflow flag.
-        const double tp = fma(sr * (xv[u][j] - mean), sp[j], 6755399441055744.0);
-        const double tq = fma(sr * (yv[u][j] - xv[u][j]), sq[j], 6755399441055744.0);
-        const int hp = __double2hiint(tp) - 0x43380000, hq = __double2hiint(tq) - 0x43380000;
-        const unsigned long long bp = ((unsigned long long)(uint32_t)hp << 32 | (uint32_t)__double2loint(tp)) + kBias;
-        const unsigned long long bq = ((unsigned long long)(uint32_t)hq << 32 | (uint32_t)__double2loint(tq)) + kBias;
-        ovf |= ((uint32_t)(bp >> 32) >= 0x10000u) | ((uint32_t)(bq >> 32) >= 0x10000u);
-        vrow[lane + 32 * j] = bp;
-        vrow[G8_N + lane + 32 * j] = bq;
-      }
-    }
-    __syncthreads();
-    // ---- phase 2: two passes of 128 (member, chunk) items per warp-half
-    unsigned char* out = planes + (size_t)blk * G8_BLOCK_BYTES;
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-      const int m = 128 * pass + 16 * warp + (lane & 15);  // 0..255: P members, then Q
-      const int ck = lane >> 4;                            // K chunk: rows 16ck..16ck+15
-      uint32_t w[G8_ND][4];
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        uint32_t vlo[4], vhi[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const unsigned long long v = vals[(16 * ck + 4 * q4 + u) * G8_VLD + m];
-          vlo[u] = (uint32_t)v;
-          vhi[u] = (uint32_t)(v >> 32);
-        }
-        // plane p (1..6) = byte (6-p) of the biased value, ^ 0x80; 4 rows per word
-        auto two_planes = [&](const uint32_t (&x)[4], uint32_t bi, uint32_t bj, uint32_t& wi, uint32_t& wj) {
-          const uint32_t sel = bi | ((bi + 4u) << 4) | (bj << 8) | ((bj + 4u) << 12);
-          const uint32_t A = __byte_perm(x[0], x[1], sel);
-          const uint32_t B = __byte_perm(x[2], x[3], sel);
-          wi = __byte_perm(A, B, 0x5410) ^ 0x80808080u;
-          wj = __byte_perm(A, B, 0x7632) ^ 0x80808080u;
-        };
-        two_planes(vhi, 1u, 0u, w[0][q4], w[1][q4]);
-        two_planes(vlo, 3u, 2u, w[2][q4], w[3][q4]);
-        two_planes(vlo, 1u, 0u, w[4][q4], w[5][q4]);
-      }
-      const int mm = m & (G8_N - 1);
-      const size_t off = (size_t)(m >= G8_N ? G8_ND * G8_PLANE : 0) + (size_t)mm * 32 +
-                         (size_t)((ck ^ ((mm >> 2) & 1)) << 4);
-#pragma unroll
-      for (int p = 0; p < G8_ND; ++p)
-        __stcs(reinterpret_cast<uint4*>(out + off + (size_t)p * G8_PLANE),
-               make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]));
-    }
-    __syncthreads();
-  }
+  for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x)
+    g8_slice_block(X, Y, idx, r, n_state, n_obs, blk, tid, sp, sq, vals, planes + (size_t)blk * G8_BLOCK_BYTES,
+                   flags, ovf, [] { __syncthreads(); });
   flags = __reduce_or_sync(0xffffffffu, flags);
   ovf = __reduce_or_sync(0xffffffffu, ovf);
   if (lane == 0) {
@@ -339,6 +358,19 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
       // B: a 64-member slice of the A planes (P'P) or the Q slices (P'Q)
       const uint32_t bbuf = qslice ? abuf + (uint32_t)(G8_ND * G8_PLANE) : abuf + (uint32_t)(q * G8_BSL);
       const uint32_t bstride = qslice ? (uint32_t)G8_BSL : (uint32_t)G8_PLANE;
+#if G8_TS
+      // A planes smem -> TMEM (columns G8_ATM + 8(p-1)); tcgen05.cp and tcgen05.mma
+      // from this thread execute in issue order, so the copy waits for the previous
+      // block's MMAs and the MMAs below see the copy.  Shared-memory reads per block
+      // drop from 26 x 6 KiB (SS operands) to 24 + 26 x 2 KiB.
+#pragma unroll
+      for (int p = 0; p < G8_ND; ++p)
+        asm volatile(
+            "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+            "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(tmem + (uint32_t)(G8_ATM + 8 * p)),
+            "l"(umma_desc_sw32(abuf + (uint32_t)(p * G8_PLANE)))
+            : "memory");
+#endif
 #pragma unroll
       for (int p = 1; p <= G8_ND; ++p) {
 #pragma unroll
@@ -346,9 +378,14 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
           if (p + qq > G8_LMAX) continue;
           const int l = p + qq;
           const bool first = first_in_period && ((p == 1) || (l > G8_ND + 1 && p == l - G8_ND));
-          const uint64_t ad = umma_desc_sw32(abuf + (uint32_t)((p - 1) * G8_PLANE));
           const uint64_t bd = umma_desc_sw32(bbuf + (uint32_t)(qq - 1) * bstride);
+#if G8_TS
+          umma_i8_ts(tmem + (uint32_t)((l - 2) * G8_NS), tmem + (uint32_t)(G8_ATM + 8 * (p - 1)), bd, idesc,
+                     first ? 0u : 1u);
+#else
+          const uint64_t ad = umma_desc_sw32(abuf + (uint32_t)((p - 1) * G8_PLANE));
           umma_i8_ss(tmem + (uint32_t)((l - 2) * G8_NS), ad, bd, idesc, first ? 0u : 1u);
+#endif
         }
       }
       umma_commit_elect(&sempty[slot]);
