@@ -17,6 +17,7 @@
 #include "localized.cuh"
 #include "l96.cuh"
 #include "gram_i8.cuh"
+#include "gram_i8_fused.cuh"
 #include "host_stream.cuh"
 
 using namespace enkf;
@@ -38,7 +39,10 @@ struct enkf_plan {
   bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
-  unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images
+  bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
+  unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
+  unsigned char* g8_ring = nullptr;       // [groups][GF_RING][48 KiB] L2-resident image ring (fused form)
+  int* g8_flags = nullptr;                // [2][groups][GF_RING] ready / consumed counters
   unsigned long long* g8_meta = nullptr;  // [256] sampled column maxima, then the overflow flag
   double* g8_partial = nullptr;           // [groups][4][128][64]
   int ws_blocks = 1, ws_ctas_per_block = 1;
@@ -197,9 +201,8 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   const int n = p->n;
   cudaError_t e = cudaSuccess;
   const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
-  if (!p->g8_planes) {
-    e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES);
-    if (e == cudaSuccess) e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2));
+  if (!p->g8_meta) {
+    e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2));
     if (e == cudaSuccess)
       e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS);
     if (e != cudaSuccess) return e;
@@ -207,7 +210,35 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   int* overflow = reinterpret_cast<int*>(p->g8_meta + 2 * G8_N);
   if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (2 * G8_N + 2), s)) != cudaSuccess) return e;
   gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, r, p->n_state, p->n_obs, p->g8_meta);
-  {
+  const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
+  if (p->gram_fused) {
+    const size_t nflags = (size_t)2 * p->g8_groups * GF_RING;
+    if (!p->g8_ring) {
+      e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GF_RING * G8_BLOCK_BYTES);
+      if (e == cudaSuccess) e = cudaMalloc(&p->g8_flags, sizeof(int) * nflags);
+      if (e != cudaSuccess) return e;
+    }
+    if ((e = cudaMemsetAsync(p->g8_flags, 0, sizeof(int) * nflags, s)) != cudaSuccess) return e;
+    const size_t smem = gram_i8_fused_smem_bytes();
+    if ((e = cudaFuncSetAttribute(gram_i8_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    int* ready = p->g8_flags;
+    int* consumed = p->g8_flags + (size_t)p->g8_groups * GF_RING;
+    int64_t n_state = p->n_state, n_obs = p->n_obs, nb = n_blocks, bpg_v = bpg;
+    const unsigned long long* cmax = p->g8_meta;
+    double* partial = p->g8_partial;
+    DevStatus* dstatus = p->dstatus;
+    unsigned char* ring = p->g8_ring;
+    void* args[] = {(void*)&X, (void*)&Y, (void*)&idx, (void*)&r, (void*)&cmax, (void*)&n_state, (void*)&n_obs,
+                    (void*)&nb, (void*)&bpg_v, (void*)&ring, (void*)&ready, (void*)&consumed, (void*)&partial,
+                    (void*)&overflow, (void*)&dstatus};
+    // cooperative: every CTA co-resident (they wait on each other through the ring)
+    e = cudaLaunchCooperativeKernel((const void*)gram_i8_fused_kernel, dim3(4 * p->g8_groups), dim3(GF_THREADS), args,
+                                    smem, s);
+    if (e != cudaSuccess) return e;
+  } else {
+    if (!p->g8_planes && (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) return e;
     const size_t smem = gram_i8_slice_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
@@ -216,15 +247,14 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
                                                                          p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                          p->dstatus);
-  }
   {
     const size_t smem = gram_i8_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
       return e;
-    const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
     gram_i8_mma_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
                                                                   p->g8_partial, overflow);
+  }
   }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
   gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
@@ -566,7 +596,10 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
-  if (const char* env = getenv("ENKF_GRAM")) p->gram_i8 = (strcmp(env, "fp64") != 0);
+  if (const char* env = getenv("ENKF_GRAM")) {
+    p->gram_i8 = (strcmp(env, "fp64") != 0);
+    p->gram_fused = (strcmp(env, "i8fused") == 0);
+  }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
   if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
@@ -641,6 +674,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->locZ);
   cudaFree(p->l96ws);
   cudaFree(p->g8_planes);
+  cudaFree(p->g8_ring);
+  cudaFree(p->g8_flags);
   cudaFree(p->g8_meta);
   cudaFree(p->g8_partial);
   cudaFree(p->cyc_status);
