@@ -45,6 +45,9 @@ constexpr int G8_BSL = G8_NS * G8_KB;             // 2 KiB: a 64-member slice of
 constexpr int G8_STAGE = G8_ND * G8_PLANE + G8_ND * G8_BSL;  // 36 KiB: A planes + B slices
 constexpr int G8_NST = 5;        // stage ring depth
 constexpr int G8_THREADS = 6 * 32;  // producer, MMA issuer, 4 flush warps
+#ifndef G8_MMA_ONLY
+#define G8_MMA_ONLY 0            // profiling only: MMAs on the first stages' data, no streaming
+#endif
 #ifndef G8_TS
 #define G8_TS 1                  // A operand (P digit planes) from TMEM (tcgen05.cp), B from smem
 #endif
@@ -329,7 +332,7 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
     // ---- producer ---------------------------------------------------------------
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)(G8_ND * G8_PLANE + (qslice ? G8_ND * G8_BSL : 0));
-      for (int64_t k = 0; k < nblk; ++k) {
+      for (int64_t k = 0; k < (G8_MMA_ONLY ? (nblk < G8_NST ? nblk : G8_NST) : nblk); ++k) {
         const int slot = (int)(k % G8_NST);
         if (k >= G8_NST) mbar_wait(&sempty[slot], (uint32_t)(((k / G8_NST) - 1) & 1));
         unsigned char* st = sm + slot * G8_STAGE;
@@ -352,7 +355,7 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
       const int slot = (int)(k % G8_NST);
       const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
       if (first_in_period && k > 0) mbar_wait(aempty, (uint32_t)(((k / G8_FLUSH_BLOCKS) - 1) & 1));
-      mbar_wait(&sfull[slot], (uint32_t)((k / G8_NST) & 1));
+      if (!G8_MMA_ONLY || k < G8_NST) mbar_wait(&sfull[slot], (uint32_t)((k / G8_NST) & 1));
       tc_fence_after();
       const uint32_t abuf = sbase + (uint32_t)(slot * G8_STAGE);
       // B: a 64-member slice of the A planes (P'P) or the Q slices (P'Q)
