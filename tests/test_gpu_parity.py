@@ -219,6 +219,33 @@ def test_analysis_vs_oracle(maker):
     assert err <= XA_TOL
 
 
+@pytest.mark.parametrize("case", list(range(16)))
+def test_random_systems_analysis(case):
+    """Acceptance-C1-style sweep (test_acceptance.py:44-61) on the whole analysis step:
+    random ensemble sizes 2..128 (N = 128 takes the int8 tensor-core Gram and anomaly
+    kernels, others the FP64 DMMA ones), n_obs log-uniform in 10..20000 (down to one
+    partial 32-row block of the int8 Gram), random sorted H, value scales spanning
+    decades; X^A against the oracle within 1e-9 and against the explicit Kalman gain."""
+    g = np.random.Generator(np.random.Philox(9000 + case))
+    n = int(g.choice([2, 3, 7, 20, 31, 64, 97, 128, 128, 128]))
+    nobs = int(np.exp(g.uniform(np.log(10), np.log(20000))))
+    ns = nobs + int(g.integers(0, 3 * nobs + 1))
+    idx = np.sort(g.choice(ns, nobs, replace=False))
+    scale = 10.0 ** g.uniform(-3, 3, ns)[:, None]
+    x = scale * (g.standard_normal((ns, 1)) + g.uniform(0.2, 2.0) * g.standard_normal((ns, n)))
+    r = (g.uniform(0.1, 2.0, nobs) * scale[idx, 0]) ** 2
+    y = x[idx].mean(axis=1, keepdims=True) + np.sqrt(r)[:, None] * g.standard_normal((nobs, n))
+    xa = P.analysis_step(x, P.ObservationBatch(y=None, perturbed=y, perturbations=None),
+                         P.SelectionOperator.from_indices(idx), r)
+    assert rel_err(xa, oracle.analysis_step(x, y, idx, r)) <= XA_TOL, (n, nobs, ns)
+    # explicit gain X + P H'(H P H' + R)^-1 (Y - H X) (test_enkf.py:215-225)
+    s = (x - x.mean(axis=1, keepdims=True)) / np.sqrt(n - 1)
+    v = s[idx]
+    k = s @ v.T @ np.linalg.inv(v @ v.T + np.diag(r)) if nobs <= 3000 else None
+    if k is not None:
+        assert rel_err(xa, x + k @ (y - x[idx])) <= 1e-8, (n, nobs, ns)
+
+
 def test_config2_cycles_open_loop():
     """Config 2: identical X^B to GPU and oracle at every cycle (open loop),
     then the GPU analysis drives the next forecast."""
