@@ -404,7 +404,6 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     asm volatile("bar.sync 1, %0;\n" ::"n"(32 * (I8_EPI_WARPS + 1)) : "memory");  // C planes in TMEM before the first MMA
     int chunk_ctr = 0;
     for (int64_t it = 0; it < my_tiles; ++it) {
-      const int buf = (int)(it % I8_NBUF);
       const int64_t tile = blockIdx.x + it * gridDim.x;
       i8_wait_a(rfull_a + 8u * (uint32_t)(it % (2 * I8_NBUF)), (uint32_t)((it / (2 * I8_NBUF)) & 1));  // the tile's row exponents
       const int* rk = rinfo + (int)(it % (2 * I8_NBUF)) * I8_TILE;

@@ -1181,7 +1181,6 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
         ec[h] = e & 7;
         m[h] = (er[h] < b && ec[h] < b) ? (er[h] == ec[h] ? 1.0 : 0.0) + PT[ec[h] * n + k0 + er[h]] : 0.0;
       }
-      bool bad = false;
 #pragma unroll
       for (int j = 0; j < LB; ++j) {
         if (j >= b) break;
@@ -1195,7 +1194,6 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
             }
             *fail = 1;
           }
-          bad = true;
           break;
         }
         const double dinv = 1.0 / d;

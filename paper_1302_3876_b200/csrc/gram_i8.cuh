@@ -36,7 +36,10 @@ constexpr int G8_N = 128;
 constexpr int G8_NS = 64;        // output columns per CTA
 constexpr int G8_KB = 32;        // observation rows per digit block (one MMA k-step)
 constexpr int G8_ND = 6;         // digits per value
-constexpr int G8_LMAX = 8;       // pairs p + q <= 8 (1-based digit index)
+#ifndef G8_LMAX_DEF
+#define G8_LMAX_DEF 8
+#endif
+constexpr int G8_LMAX = G8_LMAX_DEF;  // pairs p + q <= G8_LMAX (1-based digit index)
 constexpr int G8_NLEV = G8_LMAX - 1;
 constexpr int G8_FLUSH_BLOCKS = 512;  // 16384 rows per int32 accumulation period
 constexpr int G8_PLANE = G8_N * G8_KB;            // 4 KiB: one plane, 128 members x 32 B
@@ -51,7 +54,7 @@ constexpr int G8_THREADS = 6 * 32;  // producer, MMA issuer, 4 flush warps
 #ifndef G8_TS
 #define G8_TS 1                  // A operand (P digit planes) from TMEM (tcgen05.cp), B from smem
 #endif
-constexpr int G8_ATM = G8_NLEV * G8_NS;  // TMEM column of the A planes (after the 7 level accumulators)
+constexpr int G8_ATM = G8_NLEV * G8_NS;  // TMEM column of the A planes (after the level accumulators)
 static_assert(G8_ATM + 8 * G8_ND <= 512, "TMEM: accumulators + A planes");
 constexpr int G8_SAMPLE = 16;    // pre-pass samples every 16th observation row
 constexpr int G8_HEADROOM = 2;   // scale exponent headroom (bits) over the sampled max
@@ -96,6 +99,15 @@ __device__ __forceinline__ void umma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uin
 __device__ __forceinline__ double g8_scale(unsigned long long b) { return pow2(47 - exp_above(b) - G8_HEADROOM); }
 
 __device__ __forceinline__ double g8_sqrt_rho(double rv) { return sqrt(1.0 / rv); }
+
+// sum_l acc_l 256^(8-l) over the kept levels l = 2..G8_LMAX (v[l-2][c]), in units of
+// 256^0 at level 8: exact products, smallest level first
+__device__ __forceinline__ double g8_combine(const uint32_t (&v)[G8_NLEV][8], int c) {
+  double s = 0.0;
+#pragma unroll
+  for (int l = G8_NLEV - 1; l >= 0; --l) s = fma((double)(int)v[l][c], pow2(8 * (6 - l)), s);
+  return s;
+}
 
 // Column maxima over every G8_SAMPLE-th observation row: |P| (128) then |Q| (128),
 // as IEEE bit patterns (monotone for non-negative values).
@@ -420,10 +432,7 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double hi = fma((double)(int)v[0][c], 65536.0, fma((double)(int)v[1][c], 256.0, (double)(int)v[2][c]));
-          const double lo = fma((double)(int)v[3][c], 16777216.0,
-                                fma((double)(int)v[4][c], 65536.0, fma((double)(int)v[5][c], 256.0, (double)(int)v[6][c])));
-          acc[8 * cg + c] += fma(hi, 4294967296.0, lo);
+          acc[8 * cg + c] += g8_combine(v, c);
         }
       }
       tc_fence_before();

@@ -393,11 +393,8 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
         tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-          const double hi = fma((double)(int)v[0][c], 65536.0, fma((double)(int)v[1][c], 256.0, (double)(int)v[2][c]));
-          const double lo = fma((double)(int)v[3][c], 16777216.0,
-                                fma((double)(int)v[4][c], 65536.0, fma((double)(int)v[5][c], 256.0, (double)(int)v[6][c])));
           const int j = 8 * cg + c;
-          const double val = fma(hi, 4294967296.0, lo) * (ai / bsc[j]);
+          const double val = g8_combine(v, c) * (ai / bsc[j]);
           prow[j] = (pd == 0 ? 0.0 : prow[j]) + val;
         }
       }
