@@ -1220,7 +1220,6 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
           if (er[h] > j && ec[h] > j) m[h] -= colr[h] * colc[h] * dinv;
         }
       }
-      (void)bad;
     }
     __syncthreads();
     if (*fail) return;  // uniform
