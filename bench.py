@@ -223,6 +223,30 @@ def run_ours(args):
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
         ms = float(mt.item())
 
+    # --- the Gram's two passes timed apart (int8 form): CUDA events recorded by the
+    # library around the slice pass (the HBM-streaming pass that replaces the
+    # reference's ISM sweep) and the MMA pass, over 3 extra steps after the timed region
+    sweep_ms = None
+    n_ens_ = n
+    if n_ens_ == 128 and os.environ.get("ENKF_GRAM", "i8") == "i8":
+        import ctypes
+        from paper_1302_3876_b200 import _native
+        lib = _native.lib()
+        lib.enkf_debug_set_gram_events.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        lib.enkf_debug_gram_times.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+        handle = runner.stages.plan.handle
+        lib.enkf_debug_set_gram_events(handle, 1)
+        acc = [0.0, 0.0]
+        for _ in range(3):
+            step()
+            torch.cuda.synchronize(dev)
+            two = (ctypes.c_float * 2)()
+            if lib.enkf_debug_gram_times(handle, two) == 0:
+                acc[0] += two[0] / 3
+                acc[1] += two[1] / 3
+        lib.enkf_debug_set_gram_events(handle, 0)
+        sweep_ms = acc
+
     # --- e2e with host buffers, copies inside the timed region.  One GPU: the
     # public drop-in `analysis_step(numpy arrays)`; N GPUs: the public sharded
     # API (`distributed.ShardedAnalysis`) fed from each rank's host shard.
@@ -342,6 +366,15 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)},
         "kernels_ms": {"gram": t_gram, "allreduce": t_ar, "levels": t_lev, "anomaly": t_anom},
         "roofline": roofline,
+        "ism_sweep": None if sweep_ms is None else {
+            "kernel": "gram_i8_slice_kernel: the observation-row streaming pass of the Gram (reduced-coordinate "
+                      "ISM, DESIGN §3/§6), which replaces the reference's per-group sweeps of the Nobs x 2N panel",
+            "bound": "hbm", "unit": "GB/s", "ms": sweep_ms[0],
+            "achieved": nobs_loc * (2 * n * 8 + 16 + 2 * n * 6) / (sweep_ms[0] * 1e-3) / 1e9,
+            "peak": hbm_peak, "frac": nobs_loc * (2 * n * 8 + 16 + 2 * n * 6) / (sweep_ms[0] * 1e-3) / 1e9 / hbm_peak,
+            "algorithmic": "per observed row: read X[idx] row and Y row (2*N*8 B), r and idx (16 B), write its "
+                           "6+6 byte-digit planes (2*N*6 B) = 3600 B",
+            "mma_pass_ms": sweep_ms[1]},
         "gram_kernel": {"impl": ("gram_i8_slice_kernel + gram_i8_mma_kernel (exact byte-digit products on tcgen05 "
                                  "kind::i8; ENKF_GRAM=fp64 selects the FP64 DMMA gram128_kernel)") if gram_i8 else
                                 "gram128_kernel (FP64 DMMA)",

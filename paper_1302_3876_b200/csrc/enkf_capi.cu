@@ -40,6 +40,8 @@ struct enkf_plan {
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
+  bool g8_events = false;                 // measurement: events around the slice and MMA passes
+  cudaEvent_t g8_ev[3] = {nullptr, nullptr, nullptr};
   unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
   unsigned char* g8_ring = nullptr;       // [groups][GF_RING][48 KiB] L2-resident image ring (fused form)
   int* g8_flags = nullptr;                // [2][groups][GF_RING] ready / consumed counters
@@ -239,6 +241,11 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     if (e != cudaSuccess) return e;
   } else {
     if (!p->g8_planes && (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) return e;
+    if (p->g8_events) {
+      for (cudaEvent_t& ev : p->g8_ev)
+        if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
+      cudaEventRecord(p->g8_ev[0], s);
+    }
     const size_t smem = gram_i8_slice_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
@@ -247,6 +254,7 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
                                                                          p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                          p->dstatus);
+  if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
   {
     const size_t smem = gram_i8_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
@@ -255,6 +263,7 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram_i8_mma_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
                                                                   p->g8_partial, overflow);
   }
+  if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
   gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
@@ -675,6 +684,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->l96ws);
   cudaFree(p->g8_planes);
   cudaFree(p->g8_ring);
+  for (cudaEvent_t ev : p->g8_ev)
+    if (ev) cudaEventDestroy(ev);
   cudaFree(p->g8_flags);
   cudaFree(p->g8_meta);
   cudaFree(p->g8_partial);
@@ -1181,6 +1192,21 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, enkf::g_i8_trace, sizeof(enkf::g_i8_trace)) == cudaSuccess ? 0 : 5;
+}
+
+// Measurement-only (not part of include/enkf_b200.h): CUDA events around the
+// int8 Gram's slice pass and MMA pass (two-kernel form) of this plan.
+__attribute__((visibility("default"))) int32_t enkf_debug_set_gram_events(enkf_plan* p, int32_t on) {
+  if (!p) return ENKF_INVALID_ARGUMENT;
+  p->g8_events = on != 0;
+  return ENKF_OK;
+}
+// ms of the last slice and MMA passes (the caller has synchronised)
+__attribute__((visibility("default"))) int32_t enkf_debug_gram_times(enkf_plan* p, float* out2) {
+  if (!p || !p->g8_ev[2]) return ENKF_INVALID_ARGUMENT;
+  if (cudaEventElapsedTime(&out2[0], p->g8_ev[0], p->g8_ev[1]) != cudaSuccess) return ENKF_CUDA_ERROR;
+  if (cudaEventElapsedTime(&out2[1], p->g8_ev[1], p->g8_ev[2]) != cudaSuccess) return ENKF_CUDA_ERROR;
+  return ENKF_OK;
 }
 
 }  // extern "C"
