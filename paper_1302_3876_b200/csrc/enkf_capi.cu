@@ -232,9 +232,10 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     double* partial = p->g8_partial;
     DevStatus* dstatus = p->dstatus;
     unsigned char* ring = p->g8_ring;
+    uint32_t uz = 0;
     void* args[] = {(void*)&X, (void*)&Y, (void*)&idx, (void*)&r, (void*)&cmax, (void*)&n_state, (void*)&n_obs,
                     (void*)&nb, (void*)&bpg_v, (void*)&ring, (void*)&ready, (void*)&consumed, (void*)&partial,
-                    (void*)&overflow, (void*)&dstatus};
+                    (void*)&overflow, (void*)&dstatus, (void*)&uz};
     // cooperative: every CTA co-resident (they wait on each other through the ring)
     e = cudaLaunchCooperativeKernel((const void*)gram_i8_fused_kernel, dim3(4 * p->g8_groups), dim3(GF_THREADS), args,
                                     smem, s);
@@ -261,7 +262,7 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
         cudaSuccess)
       return e;
     gram_i8_mma_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
-                                                                  p->g8_partial, overflow);
+                                                                  p->g8_partial, overflow, 0u);
   }
   if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   }

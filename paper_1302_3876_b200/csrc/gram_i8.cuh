@@ -95,6 +95,191 @@ __device__ __forceinline__ void umma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uin
       : "memory");
 }
 
+// The same issue sequence as one PTX block (G8_TS): one elect for the 6 copies
+// and 26 MMAs of a block; generated for G8_ND = 6, G8_LMAX = 8, G8_ATM = 448.
+__device__ __forceinline__ void g8_issue_block_asm(uint32_t uz, uint64_t a0, uint64_t b0, uint64_t bst16,
+                                                   uint32_t acc_first) {
+  asm volatile(
+        "{\n"
+        ".reg .pred e, pa, pt;\n"
+        ".reg .b64 ad, bd;\n"
+        ".reg .b32 dt, at;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "setp.ne.b32 pa, %3, 0;\n"
+        "setp.eq.b32 pt, %4, %4;\n"
+        "add.u64 ad, %0, 0;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "add.u64 ad, %0, 256;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "add.u64 ad, %0, 512;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "add.u64 ad, %0, 768;\n"
+        "add.u32 at, %4, 472;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "add.u64 ad, %0, 1024;\n"
+        "add.u32 at, %4, 480;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "add.u64 ad, %0, 1280;\n"
+        "add.u32 at, %4, 488;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 0;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 64;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 2, %1;\n"
+        "add.u32 dt, %4, 128;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 3, %1;\n"
+        "add.u32 dt, %4, 192;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 4, %1;\n"
+        "add.u32 dt, %4, 256;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 5, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 448;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 64;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 128;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 2, %1;\n"
+        "add.u32 dt, %4, 192;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 3, %1;\n"
+        "add.u32 dt, %4, 256;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 4, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 5, %1;\n"
+        "add.u32 dt, %4, 384;\n"
+        "add.u32 at, %4, 456;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 128;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 192;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 2, %1;\n"
+        "add.u32 dt, %4, 256;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 3, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 4, %1;\n"
+        "add.u32 dt, %4, 384;\n"
+        "add.u32 at, %4, 464;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 192;\n"
+        "add.u32 at, %4, 472;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 256;\n"
+        "add.u32 at, %4, 472;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 2, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 472;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 3, %1;\n"
+        "add.u32 dt, %4, 384;\n"
+        "add.u32 at, %4, 472;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 256;\n"
+        "add.u32 at, %4, 480;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 480;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 2, %1;\n"
+        "add.u32 dt, %4, 384;\n"
+        "add.u32 at, %4, 480;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 0, %1;\n"
+        "add.u32 dt, %4, 320;\n"
+        "add.u32 at, %4, 488;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "mad.lo.u64 bd, %2, 1, %1;\n"
+        "add.u32 dt, %4, 384;\n"
+        "add.u32 at, %4, 488;\n"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
+        "}\n"
+        ::"l"(a0), "l"(b0), "l"(bst16), "r"(acc_first), "r"(uz), "r"(uz + idesc_g8())
+        : "memory");
+}
+
+// Issue one 32-row block: the six A planes smem -> TMEM (columns G8_ATM + 8(p-1);
+// tcgen05.cp and tcgen05.mma from one thread execute in issue order, so the copy
+// waits for the previous block's MMAs and the MMAs see the copy — shared-memory
+// reads per block drop from 26 x 6 KiB (SS operands) to 24 + 26 x 2 KiB) and the
+// digit-pair MMAs into the level accumulators (columns 64(l-2)).  TMEM addresses
+// are compile-time offsets from `uz` (a kernel parameter equal to 0: the CTA owns
+// all 512 columns, so its allocation starts at column 0) and the descriptors are
+// one base per operand plus constants, so the operands stay on the uniform datapath.
+__device__ __forceinline__ void g8_issue_block(uint32_t uz, uint32_t abuf, uint32_t bbuf, uint32_t bstride,
+                                               bool first_in_period) {
+  const uint64_t a0 = umma_desc_sw32(abuf);
+  const uint64_t b0 = umma_desc_sw32(bbuf);
+#if G8_TS && G8_LMAX_DEF == 8
+  static_assert(G8_ND == 6 && G8_NS == 64 && G8_ATM == 448, "g8_issue_block_asm is generated for this shape");
+  g8_issue_block_asm(uz, a0, b0, (uint64_t)(bstride >> 4), first_in_period ? 0u : 1u);
+  return;
+#endif
+  const uint32_t idesc = uz + idesc_g8();
+#if G8_TS
+#pragma unroll
+  for (int p = 0; p < G8_ND; ++p)
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(uz + (uint32_t)(G8_ATM + 8 * p)),
+        "l"(a0 + (uint64_t)((p * G8_PLANE) >> 4))
+        : "memory");
+#endif
+#pragma unroll
+  for (int p = 1; p <= G8_ND; ++p) {
+#pragma unroll
+    for (int qq = 1; qq <= G8_ND; ++qq) {
+      if (p + qq > G8_LMAX) continue;
+      const int l = p + qq;
+      const bool first = first_in_period && ((p == 1) || (l > G8_ND + 1 && p == l - G8_ND));
+      const uint64_t bd = b0 + (uint64_t)(((uint32_t)(qq - 1) * bstride) >> 4);
+#if G8_TS
+      umma_i8_ts(uz + (uint32_t)((l - 2) * G8_NS), uz + (uint32_t)(G8_ATM + 8 * (p - 1)), bd, idesc,
+                 first ? 0u : 1u);
+#else
+      umma_i8_ss(uz + (uint32_t)((l - 2) * G8_NS), a0 + (uint64_t)(((p - 1) * G8_PLANE) >> 4), bd, idesc,
+                 first ? 0u : 1u);
+#endif
+    }
+  }
+}
+
 // 2^(47 - e - headroom) for a column whose sampled max|.| has IEEE bits b
 __device__ __forceinline__ double g8_scale(unsigned long long b) { return pow2(47 - exp_above(b) - G8_HEADROOM); }
 
@@ -301,7 +486,7 @@ gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 __global__ void __launch_bounds__(G8_THREADS, 1)
 gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long long* __restrict__ cmax,
                    int64_t n_blocks, int64_t blocks_per_group, double* __restrict__ partial,
-                   const int* __restrict__ overflow) {
+                   const int* __restrict__ overflow, uint32_t uz /* = 0 */) {
   if (*overflow) return;  // the FP64 fallback computes the Gram
   extern __shared__ __align__(1024) unsigned char g8sm_raw[];
   unsigned char* sm = g8sm_raw + ((1024u - (smem_u32(g8sm_raw) & 1023u)) & 1023u);
@@ -338,7 +523,8 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t tmem = 0;  // one CTA per SM owns all 512 columns
+  if (tid == 0 && *tmem_slot != 0u) __trap();
 
   if (warp == 0) {
     // ---- producer ---------------------------------------------------------------
@@ -362,7 +548,6 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
   } else if (warp == 1) {
     // ---- MMA issuer ---------------------------------------------------------------
     const uint32_t sbase = smem_u32(sm);
-    const uint32_t idesc = idesc_g8();
     for (int64_t k = 0; k < nblk; ++k) {
       const int slot = (int)(k % G8_NST);
       const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
@@ -373,36 +558,7 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
       // B: a 64-member slice of the A planes (P'P) or the Q slices (P'Q)
       const uint32_t bbuf = qslice ? abuf + (uint32_t)(G8_ND * G8_PLANE) : abuf + (uint32_t)(q * G8_BSL);
       const uint32_t bstride = qslice ? (uint32_t)G8_BSL : (uint32_t)G8_PLANE;
-#if G8_TS
-      // A planes smem -> TMEM (columns G8_ATM + 8(p-1)); tcgen05.cp and tcgen05.mma
-      // from this thread execute in issue order, so the copy waits for the previous
-      // block's MMAs and the MMAs below see the copy.  Shared-memory reads per block
-      // drop from 26 x 6 KiB (SS operands) to 24 + 26 x 2 KiB.
-#pragma unroll
-      for (int p = 0; p < G8_ND; ++p)
-        asm volatile(
-            "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-            "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(tmem + (uint32_t)(G8_ATM + 8 * p)),
-            "l"(umma_desc_sw32(abuf + (uint32_t)(p * G8_PLANE)))
-            : "memory");
-#endif
-#pragma unroll
-      for (int p = 1; p <= G8_ND; ++p) {
-#pragma unroll
-        for (int qq = 1; qq <= G8_ND; ++qq) {
-          if (p + qq > G8_LMAX) continue;
-          const int l = p + qq;
-          const bool first = first_in_period && ((p == 1) || (l > G8_ND + 1 && p == l - G8_ND));
-          const uint64_t bd = umma_desc_sw32(bbuf + (uint32_t)(qq - 1) * bstride);
-#if G8_TS
-          umma_i8_ts(tmem + (uint32_t)((l - 2) * G8_NS), tmem + (uint32_t)(G8_ATM + 8 * (p - 1)), bd, idesc,
-                     first ? 0u : 1u);
-#else
-          const uint64_t ad = umma_desc_sw32(abuf + (uint32_t)((p - 1) * G8_PLANE));
-          umma_i8_ss(tmem + (uint32_t)((l - 2) * G8_NS), ad, bd, idesc, first ? 0u : 1u);
-#endif
-        }
-      }
+      g8_issue_block(uz, abuf, bbuf, bstride, first_in_period);
       umma_commit_elect(&sempty[slot]);
       if ((k % G8_FLUSH_BLOCKS) == G8_FLUSH_BLOCKS - 1 || k == nblk - 1) umma_commit_elect(afull);
       __syncwarp();

@@ -77,7 +77,7 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
                      const double* __restrict__ r, const unsigned long long* __restrict__ cmax, int64_t n_state,
                      int64_t n_obs, int64_t n_blocks, int64_t blocks_per_group, unsigned char* __restrict__ ring,
                      int* __restrict__ ready, int* __restrict__ consumed, double* __restrict__ partial,
-                     int* __restrict__ overflow, DevStatus* __restrict__ status) {
+                     int* __restrict__ overflow, DevStatus* __restrict__ status, uint32_t uz /* = 0 */) {
   extern __shared__ __align__(1024) unsigned char gfsm_raw[];
   unsigned char* sm = gfsm_raw + ((1024u - (smem_u32(gfsm_raw) & 1023u)) & 1023u);
   unsigned char* stages = sm;                                        // [GF_NST][G8_STAGE]
@@ -132,7 +132,8 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  constexpr uint32_t tmem = 0;  // one CTA per SM owns all 512 columns
+  if (tid == 0 && *tmem_slot != 0u) __trap();
 
   // this CTA slices blocks t = q, q + 4, ... of its group, two 16-row halves each
   const int64_t my_blocks = nblk > q ? (nblk - 1 - q) / 4 + 1 : 0;
@@ -340,7 +341,6 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   } else if (warp == MMAW) {
     // ---- MMA issuer (as gram_i8_mma_kernel, A planes from TMEM) -------------------
     const uint32_t sbase = smem_u32(stages);
-    const uint32_t idesc = idesc_g8();
     for (int64_t k = 0; k < nblk; ++k) {
       const int st = (int)(k % GF_NST);
       const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
@@ -350,25 +350,7 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
       const uint32_t abuf = sbase + (uint32_t)(st * G8_STAGE);
       const uint32_t bbuf = qslice ? abuf + (uint32_t)(G8_ND * G8_PLANE) : abuf + (uint32_t)(q * G8_BSL);
       const uint32_t bstride = qslice ? (uint32_t)G8_BSL : (uint32_t)G8_PLANE;
-#pragma unroll
-      for (int p = 0; p < G8_ND; ++p)
-        asm volatile(
-            "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-            "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(tmem + (uint32_t)(G8_ATM + 8 * p)),
-            "l"(umma_desc_sw32(abuf + (uint32_t)(p * G8_PLANE)))
-            : "memory");
-#pragma unroll
-      for (int p = 1; p <= G8_ND; ++p) {
-#pragma unroll
-        for (int qq = 1; qq <= G8_ND; ++qq) {
-          if (p + qq > G8_LMAX) continue;
-          const int l = p + qq;
-          const bool first = first_in_period && ((p == 1) || (l > G8_ND + 1 && p == l - G8_ND));
-          const uint64_t bd = umma_desc_sw32(bbuf + (uint32_t)(qq - 1) * bstride);
-          umma_i8_ts(tmem + (uint32_t)((l - 2) * G8_NS), tmem + (uint32_t)(G8_ATM + 8 * (p - 1)), bd, idesc,
-                     first ? 0u : 1u);
-        }
-      }
+      g8_issue_block(uz, abuf, bbuf, bstride, first_in_period);
       umma_commit_elect(&sempty[st]);
       if ((k % G8_FLUSH_BLOCKS) == G8_FLUSH_BLOCKS - 1 || k == nblk - 1) umma_commit_elect(afull);
       __syncwarp();

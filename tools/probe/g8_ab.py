@@ -1,7 +1,7 @@
 """A/B of the level-0 Gram: FP64 DMMA (gram128) vs the int8-digit tensor-core
 path (ENKF_GRAM=i8), timed with CUDA events, results compared.
 
-    python tools/probe/g8_ab.py [log2_obs] [log2_state] [reps]
+    python tools/probe/g8_ab.py [log2_obs] [log2_state] [reps] [modes, default fp64,i8]
 """
 import ctypes
 import json
@@ -16,6 +16,7 @@ from paper_1302_3876_b200 import _native  # noqa: E402
 lg_o = int(sys.argv[1]) if len(sys.argv) > 1 else 20
 lg_s = int(sys.argv[2]) if len(sys.argv) > 2 else lg_o + 3
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+modes = sys.argv[4].split(",") if len(sys.argv) > 4 else ["fp64", "i8"]
 dev = torch.device("cuda", 0)
 lib = _native.lib()
 s = torch.cuda.current_stream().cuda_stream
@@ -30,7 +31,7 @@ y = x[idx].mean(dim=1, keepdim=True) + torch.randn((no, n), dtype=torch.float64,
 r = 0.25 + 0.75 * torch.rand((no,), dtype=torch.float64, device=dev, generator=g)
 out = {"n_obs": no, "n_state": ns}
 grams = {}
-for mode in ("fp64", "i8"):
+for mode in modes:
     os.environ["ENKF_GRAM"] = mode
     plan = _native.Plan(ns, no, n, 0)
     gram = torch.empty((n, 2 * n), dtype=torch.float64, device=dev)
@@ -50,7 +51,7 @@ for mode in ("fp64", "i8"):
     grams[mode] = gram.clone()
     out[mode + "_ms"] = sorted(ts)
     del plan
-d = (grams["i8"] - grams["fp64"]).abs().max().item() / grams["fp64"].abs().max().item()
-out["max_rel_diff"] = d
-out["sym"] = (grams["i8"][:, :n] - grams["i8"][:, :n].T).abs().max().item()
+for mode in modes[1:]:
+    out[mode + "_max_rel_diff"] = (grams[mode] - grams[modes[0]]).abs().max().item() / grams[modes[0]].abs().max().item()
+    out[mode + "_sym"] = (grams[mode][:, :n] - grams[mode][:, :n].T).abs().max().item()
 print(json.dumps(out))
