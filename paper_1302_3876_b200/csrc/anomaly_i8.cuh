@@ -38,6 +38,9 @@ constexpr int I8_CHUNK = I8_CHUNK_ROWS;  // rows per MMA (N of the instruction)
 // 32-row buffer (N = 32 halves the MMA count; the epilogue drains before reuse)
 constexpr int I8_ABUF = I8_CHUNK == 16 ? 2 : 1;
 constexpr int I8_ND = 6;          // byte digits per value
+#ifndef I8_TBAL
+#define I8_TBAL 0   // balanced (zero-mean) digits for T: the p+q > I8_LMAX truncation is then unbiased
+#endif
 #ifndef I8_LMAX_DEF
 #define I8_LMAX_DEF 8
 #endif
@@ -384,7 +387,7 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     // (T = I + (I - 11'/N) A / sqrt(N-1) from the levels kernel)
     auto cval = [&](int k) { return T[k * I8_N + j]; };
     if (half == 0) {
-      const double cscale = pow2(47 - fT);
+      const double cscale = pow2(I8_TBAL ? 46 - fT : 47 - fT);
 #pragma unroll 1
       for (int p = 0; p < I8_ND; ++p) {
 #pragma unroll 1
@@ -392,8 +395,14 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
           uint32_t word = 0;
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
+#if I8_TBAL
+            // balanced digits of T (bytes of W + 0x808080808080, each ^ 0x80; |W| <= 2^46)
+            const long long v = round_scaled(cval(i8_kperm(w, b)), cscale) + 0x808080808080ll;
+            word |= (byte_of(v, 5 - p) ^ 0x80u) << (8 * b);
+#else
             const long long v = round_scaled(cval(i8_kperm(w, b)), cscale);
             word |= byte_of(v, 5 - p) << (8 * b);
+#endif
           }
           tmem_st1(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(32 * p + w), word);
         }
@@ -517,7 +526,8 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
                 const int l = p + q;
                 // the first pair of level l (at k-step 0) overwrites the accumulator
                 const bool first = ks == 0 && ((p == 1) || (l > I8_ND + 1 && p == l - I8_ND));
-                const uint32_t idesc = uz + idesc_i8(q == 1, p == 1);  // A = C digits (q), B = X digits (p)
+                // A = C digits (q: all signed when balanced), B = X digits (p: top one signed)
+                const uint32_t idesc = uz + idesc_i8(I8_TBAL ? true : q == 1, p == 1);
                 const uint64_t bdesc = desc0 + (uint64_t)(((p - 1) * I8_PLANE_BYTES + 32 * ks) >> 4);
                 const uint32_t atm = uz + (uint32_t)(32 * (q - 1) + 8 * ks);
                 umma_i8_ts(dacc + (uint32_t)((l - 2) * I8_CHUNK), atm, bdesc, idesc, first ? 0u : 1u);
@@ -535,7 +545,8 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
     }
   } else {
     // ---- slicer warps: rows 16w .. 16w+15 of each tile, from the smem stage ----
-    const int kbias = fT - 1072;  // k = e + fT - 50 with e = bc - 1022
+    // k = e + fT - 50 with e = bc - 1022 (T scale 2^(47-fT)); one more with balanced T digits
+    const int kbias = fT - (I8_TBAL ? 1071 : 1072);
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int buf = (int)(it % I8_NBUF);
       i8_wait_a(sfull_a + 8u * (uint32_t)(buf), (uint32_t)((it / I8_NBUF) & 1));
