@@ -799,6 +799,16 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_obs, cudaEventDisableTiming), st);
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_anom, cudaEventDisableTiming), st);
   }
+  // On any early return below, wait for the copies already queued: the caller's
+  // buffers must not be touched by DMA or kernels after the call returns.
+  struct Drain {
+    cudaStream_t a, b, c;
+    ~Drain() {
+      cudaStreamSynchronize(a);
+      cudaStreamSynchronize(b);
+      cudaStreamSynchronize(c);
+    }
+  } drain{s, p->hs_in, p->hs_out};
   int64_t chunk_rows = (int64_t)(p->host_chunk_bytes / row_bytes);
   if (chunk_rows < 1024) chunk_rows = 1024;
   const int64_t nchunks = (p->n_state + chunk_rows - 1) / chunk_rows;
@@ -851,10 +861,7 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
   mark(3, s);  // T ready
   {
     int rc = enkf_plan_sync_status(p, s, st);
-    if (rc != ENKF_OK) {
-      cudaStreamSynchronize(p->hs_in);  // the caller's X must not be read after return
-      return rc;
-    }
+    if (rc != ENKF_OK) return rc;  // (Drain waits for the X copies in flight)
   }
   // 3b. anomaly update chunk by chunk (in place), X^A out
   for (int64_t c = 0; c < nchunks; ++c) {
