@@ -917,6 +917,10 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     if (Xmap && is_pinned(XA_h))
       return analysis_host_streamed(p, X_h, (const double*)Xmap, Y_h, idx_h, r_h, XA_h, st);
   }
+  struct Drain {
+    cudaStream_t a;
+    ~Drain() { cudaStreamSynchronize(a); }
+  } drain{s};  // no queued copy outlives the call, on any return path
   CUDA_TRY(copy_h2d(p, p->hx, X_h, sizeof(double) * (size_t)p->n_state * n, s), st);
   CUDA_TRY(copy_h2d(p, p->hy, Y_h, sizeof(double) * (size_t)p->n_obs * n, s), st);
   CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
