@@ -56,7 +56,13 @@ constexpr int G8_THREADS = 6 * 32;  // producer, MMA issuer, 4 flush warps
 #endif
 constexpr int G8_ATM = G8_NLEV * G8_NS;  // TMEM column of the A planes (after the level accumulators)
 static_assert(G8_ATM + 8 * G8_ND <= 512, "TMEM: accumulators + A planes");
-constexpr int G8_SAMPLE = 16;    // pre-pass samples every 16th observation row
+constexpr int G8_SAMPLE = 16;    // pre-pass samples every 16th observation row at least ...
+constexpr int64_t G8_SAMPLES_MAX = 1 << 17;  // ... and at most ~128K rows (sparser for large n_obs)
+__host__ __device__ inline int64_t g8_sample_stride(int64_t n_obs) {
+  int64_t st = G8_SAMPLE;
+  while ((n_obs + st - 1) / st > G8_SAMPLES_MAX) st *= 2;
+  return st;
+}
 constexpr int G8_HEADROOM = 2;   // scale exponent headroom (bits) over the sampled max
 constexpr int G8_SLICE_THREADS = 256;
 constexpr int G8_VLD = 2 * G8_N + 1;  // slice-kernel staging row stride (uint64)
@@ -294,7 +300,8 @@ __device__ __forceinline__ double g8_combine(const uint32_t (&v)[G8_NLEV][8], in
   return s;
 }
 
-// Column maxima over every G8_SAMPLE-th observation row: |P| (128) then |Q| (128),
+// Column maxima over every g8_sample_stride(n_obs)-th observation row (16th, or
+// sparser so that ~128K rows are sampled): |P| (128) then |Q| (128),
 // as IEEE bit patterns (monotone for non-negative values).
 __global__ void __launch_bounds__(256) gram_i8_scales_kernel(const double* __restrict__ X,
                                                              const double* __restrict__ Y,
@@ -306,26 +313,46 @@ __global__ void __launch_bounds__(256) gram_i8_scales_kernel(const double* __res
   for (int e = tid; e < 2 * G8_N; e += blockDim.x) red[e] = 0ull;
   __syncthreads();
   double mp[4] = {0, 0, 0, 0}, mq[4] = {0, 0, 0, 0};
-  const int64_t nsamp = (n_obs + G8_SAMPLE - 1) / G8_SAMPLE;
-  for (int64_t sidx = blockIdx.x * 8 + warp; sidx < nsamp; sidx += (int64_t)gridDim.x * 8) {
-    const int64_t k = sidx * G8_SAMPLE;
-    const int64_t src = idx ? idx[k] : k;
-    if (src < 0 || src >= n_state) continue;  // flagged by the slice kernel
-    const double rv = r[k];
-    if (!(rv > 0.0) || !isfinite(rv)) continue;
-    const double sr = g8_sqrt_rho(rv);
-    double xv[4], yv[4], s = 0.0;
+  const int64_t stride = g8_sample_stride(n_obs);
+  const int64_t nsamp = (n_obs + stride - 1) / stride;
+  // 4 samples per warp in flight (independent idx -> row loads)
+  constexpr int U = 4;
+  const int64_t wstride = (int64_t)gridDim.x * 8;
+  for (int64_t s0 = blockIdx.x * 8 + warp; s0 < nsamp; s0 += U * wstride) {
+    int64_t src[U], k[U];
+    double rv[U];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      xv[m] = X[src * G8_N + lane + 32 * m];
-      yv[m] = Y[k * G8_N + lane + 32 * m];
-      s += xv[m];
+    for (int u = 0; u < U; ++u) {
+      const int64_t sidx = s0 + u * wstride;
+      k[u] = sidx * stride;
+      src[u] = -1;
+      rv[u] = 0.0;
+      if (sidx < nsamp) {
+        src[u] = idx ? idx[k[u]] : k[u];
+        rv[u] = r[k[u]];
+      }
     }
-    const double mean = warp_sum(s) * (1.0 / G8_N);
+    double xv[U][4], yv[U][4];
+    bool ok[U];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      mp[m] = fmax(mp[m], fabs(sr * (xv[m] - mean)));
-      mq[m] = fmax(mq[m], fabs(sr * (yv[m] - xv[m])));
+    for (int u = 0; u < U; ++u) {
+      // invalid samples (bad index, r <= 0, non-finite r) are skipped: flagged by the slice kernel
+      ok[u] = src[u] >= 0 && src[u] < n_state && rv[u] > 0.0 && isfinite(rv[u]);
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        xv[u][m] = ok[u] ? X[src[u] * G8_N + lane + 32 * m] : 0.0;
+        yv[u][m] = ok[u] ? Y[k[u] * G8_N + lane + 32 * m] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double mean = warp_sum((xv[u][0] + xv[u][1]) + (xv[u][2] + xv[u][3])) * (1.0 / G8_N);
+      const double sr = ok[u] ? g8_sqrt_rho(rv[u]) : 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        mp[m] = fmax(mp[m], fabs(sr * (xv[u][m] - mean)));
+        mq[m] = fmax(mq[m], fabs(sr * (yv[u][m] - xv[u][m])));
+      }
     }
   }
 #pragma unroll
