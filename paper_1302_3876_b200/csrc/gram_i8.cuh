@@ -478,7 +478,10 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
 
 // Slice pass (two-kernel form, ENKF_GRAM=i8split): every 32-row block -> its
 // operand image in HBM.
-__global__ void __launch_bounds__(G8_SLICE_THREADS)
+#ifndef G8_SLICE_MINB
+#define G8_SLICE_MINB 1
+#endif
+__global__ void __launch_bounds__(G8_SLICE_THREADS, G8_SLICE_MINB)
 gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int64_t* __restrict__ idx,
                      const double* __restrict__ r, const unsigned long long* __restrict__ cmax, int64_t n_state,
                      int64_t n_obs, int64_t n_blocks, unsigned char* __restrict__ planes, int* __restrict__ overflow,
