@@ -104,7 +104,10 @@ int32_t enkf_plan_sync_status(enkf_plan* plan, void* stream, enkf_status* status
 int32_t enkf_plan_reset_status(enkf_plan* plan, void* stream);
 
 /* Full analysis step on HOST buffers: copies X, Y, idx, r in, runs the step,
- * copies XA out.  Pinned host memory is used at full PCIe speed. */
+ * copies XA out; returns after every copy has completed.  With page-locked X and
+ * XA (and idx given) the call streams: X[idx] gathered over PCIe, the Gram pass,
+ * then X chunks in and XA chunks out concurrently.  Pageable buffers go through
+ * a pinned staging ring. */
 int32_t enkf_analysis_host_f64(enkf_plan* plan, const double* X_h, const double* Y_h,
                                const int64_t* idx_h, const double* r_h, double* XA_h,
                                enkf_status* status);

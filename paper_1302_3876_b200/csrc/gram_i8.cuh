@@ -476,7 +476,7 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
   sync();
 }
 
-// Slice pass (two-kernel form, ENKF_GRAM=i8split): every 32-row block -> its
+// Slice pass of the (default) two-kernel form: every 32-row block -> its
 // operand image in HBM.
 #ifndef G8_SLICE_MINB
 #define G8_SLICE_MINB 1
