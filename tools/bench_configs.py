@@ -103,16 +103,56 @@ def time_cycled(cycles=100, cpu_cycles=5):
                                "cpu_threads": os.cpu_count(), "note": "wall clock incl. one sync per 100 cycles"}}
 
 
+def time_localized(reps=5):
+    """Localized analysis (enkf.py:193-199): GPU matrix-free cyclic
+    influence (taper evaluated in-kernel), GPU with the dense influence matrix, and the
+    CPU oracle with the dense matrix, on a small, a config-2-sized and a larger case."""
+    out = {}
+    cases = [("l96_40", 40, 20, 20, 10.0), ("l96_4096", 4096, 64, 2048, 50.0), ("ns65536", 1 << 16, 128, 1 << 13, 500.0)]
+    for name, ns, nens, nobs, scale in cases:
+        rng = np.random.Generator(np.random.Philox(ns + nens))
+        x = rng.standard_normal((ns, nens)) * rng.uniform(0.5, 2.0, (ns, 1)) + rng.standard_normal((ns, 1))
+        idx = np.sort(rng.choice(ns, size=nobs, replace=False))
+        r = rng.uniform(0.25, 1.0, nobs)
+        pert = x[idx].mean(axis=1)[:, None] + rng.standard_normal((nobs, nens))
+        h = P.SelectionOperator.from_indices(idx)
+        obs = P.ObservationBatch(y=None, perturbed=pert, perturbations=None)
+        lazy = P.influence_matrix_cyclic(ns, h, scale=scale)
+        dense = np.asarray(lazy)
+        dev = torch.device("cuda", 0)
+        xd, rd = torch.from_numpy(x).to(dev), torch.from_numpy(r).to(dev)
+        obs_d = P.ObservationBatch(y=None, perturbed=torch.from_numpy(pert).to(dev), perturbations=None)
+        dd = torch.from_numpy(dense).to(dev)
+        res = {"shape": {"n_state": ns, "n_ens": nens, "n_obs": nobs, "scale": scale}}
+        for key, loc in (("gpu_matrix_free_ms", lazy), ("gpu_dense_ms", dd)):
+            P.analysis_step(xd, obs_d, h, rd, "sherman", localization=loc)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                xa = P.analysis_step(xd, obs_d, h, rd, "sherman", localization=loc)
+            torch.cuda.synchronize()
+            res[key] = (time.perf_counter() - t0) / reps * 1e3
+        t0 = time.perf_counter()
+        ref = oracle.analysis_step_localized(x, pert, idx, r, dense)
+        res["cpu_oracle_dense_ms"] = (time.perf_counter() - t0) * 1e3
+        res["xa_rel_err_vs_oracle"] = float(np.abs(xa.cpu().numpy() - ref).max() / np.abs(ref).max())
+        out[name] = res
+    return {"localized": out}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--cycled", action="store_true", help="also time the config-2 closed loop")
+    ap.add_argument("--localized", action="store_true", help="also time the localized analysis (row f4)")
     a = ap.parse_args()
     out = {}
     if a.cycled:
         print(json.dumps(time_cycled()), flush=True)
-    for cfg in [int(c) for c in a.configs.split(",")]:
+    if a.localized:
+        print(json.dumps(time_localized()), flush=True)
+    for cfg in [int(c) for c in a.configs.split(",") if c]:
         p = problem(cfg)
         reps = a.reps if cfg < 4 else 3
         dev_s, dev_wall = time_device(p, reps)
