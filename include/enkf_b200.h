@@ -22,6 +22,7 @@
  *                           (enkf.py:138-164) evaluated on the fly (matrix-free)
  *   enkf_forecast_l96_f64   models/lorenz96.py:31-78  Lorenz96.advance (RK4 steps), bit-exact
  *   enkf_cycle_l96_f64      experiment.py:457-479     forecast -> (inflation) -> analysis cycles, device-resident
+ *   enkf_cycle_l96_localized_f64 experiment.py:457-479 the same with the localized (cyclic taper) analysis
  *   enkf_inflate_f64        enkf.py:123-135           inflate (covariance inflation about the row mean)
  *
  * Layouts (all fp64 row-major, the reference's C-order arrays):
@@ -144,6 +145,14 @@ int32_t enkf_cycle_l96_f64(enkf_plan* plan, double* X, const double* Ys, const i
                            int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing, double inflation,
                            double* mean_f, double* mean_a, void* stream, enkf_status* status,
                            int32_t* failed_cycle);
+/* The same loop with the localized analysis (experiment.py:470-473 with
+ * localization = influence_matrix_cyclic(n_state, h, loc_scale), enkf.py:138-164,
+ * 193-199), the taper evaluated in-kernel — the lorenz-small preset's loop.
+ * loc_scale <= 0 -> INVALID_ARGUMENT. */
+int32_t enkf_cycle_l96_localized_f64(enkf_plan* plan, double* X, const double* Ys, const int64_t* idx,
+                                     const double* r, int32_t n_cycles, int32_t steps_per_cycle, double dt,
+                                     double forcing, double inflation, double loc_scale, double* mean_f,
+                                     double* mean_a, void* stream, enkf_status* status, int32_t* failed_cycle);
 /* Covariance inflation (enkf.py:123-135): Xout = mean + alpha (X - mean) per row of the
  * [n_rows][n_ens] ensemble (X may alias Xout); alpha < 1 -> INVALID_ARGUMENT, alpha == 1 copies. */
 int32_t enkf_inflate_f64(const double* X, double* Xout, int64_t n_rows, int64_t n_ens, double alpha,

@@ -271,17 +271,21 @@ def inflate(x, alpha):
     return mean + alpha * (x - mean)
 
 
-def cycle_l96(x0, ys, indices, r, steps_per_cycle, dt=0.05, forcing=8.0, inflation=1.0):
+def cycle_l96(x0, ys, indices, r, steps_per_cycle, dt=0.05, forcing=8.0, inflation=1.0,
+              localization_scale=None):
     """experiment.py:457-479 closed loop with the lorenz96 model: forecast
-    (enkf.py:202-212), inflation when > 1 (:466-467), then analysis_step, per
-    cycle; returns the final ensemble and the forecast / analysis ensemble means."""
+    (enkf.py:202-212), inflation when > 1 (:466-467), then analysis_step — with
+    the cyclic influence matrix of enkf.py:138-164 when ``localization_scale`` is
+    given (experiment.py:470-473, the lorenz-small preset) — per cycle; returns the
+    final ensemble and the forecast / analysis ensemble means."""
     x = np.asarray(x0, dtype=float)
+    delta = None if localization_scale is None else influence_matrix_cyclic(x.shape[0], indices, localization_scale)
     mean_f, mean_a = [], []
     for y in ys:
         x = l96_advance(x, steps_per_cycle, dt, forcing)
         mean_f.append(x.mean(axis=1))
         if inflation > 1.0:
             x = inflate(x, inflation)
-        x = analysis_step(x, y, indices, r)
+        x = analysis_step(x, y, indices, r) if delta is None else analysis_step_localized(x, y, indices, r, delta)
         mean_a.append(x.mean(axis=1))
     return x, np.stack(mean_f), np.stack(mean_a)

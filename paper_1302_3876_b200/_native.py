@@ -64,6 +64,9 @@ PROTOTYPES = {
     "enkf_forecast_l96_f64": (_i32, [_vp, _vp, _vp, ctypes.c_double, ctypes.c_double, _i32, _vp, _st]),
     "enkf_cycle_l96_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_double, _vp, _vp, _vp, _st, ctypes.POINTER(_i32)]),
+    "enkf_cycle_l96_localized_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _i32, _i32, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _st,
+                                            ctypes.POINTER(_i32)]),
     "enkf_inflate_f64": (_i32, [_vp, _vp, _i64, _i64, ctypes.c_double, _vp]),
 }
 

@@ -978,6 +978,50 @@ int32_t enkf_innovations_f64(const double* X, const double* Y, const int64_t* id
 
 namespace {
 // Shared body of the two localized entry points (enkf.py:187-199).
+// The launches of one localized analysis (enkf.py:187-199) on stream s, flags into
+// p->dstatus: V, D rows; Gram -> levels -> Z; X + (Delta o (S V')) Z.  XA may alias X
+// (each CTA of the update kernel reads and writes only its own state rows).
+cudaError_t launch_localized(enkf_plan* p, const double* X, const double* Y, const int64_t* idx, const double* r,
+                             const double* delta, double scale, int mode, double* XA, cudaStream_t s) {
+  const int n = p->n;
+  const size_t obs_elems = (size_t)p->n_obs * (size_t)n;
+  cudaError_t e = cudaSuccess;
+  if (!p->locV && obs_elems) {
+    if ((e = cudaMalloc(&p->locV, sizeof(double) * obs_elems)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->locD, sizeof(double) * obs_elems)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&p->locZ, sizeof(double) * obs_elems)) != cudaSuccess) return e;
+  }
+  const double root = std::sqrt((double)n - 1.0);
+  if (p->n_obs > 0) {
+    const int64_t threads = p->n_obs * 32;
+    obs_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(X, Y, idx, p->locV, p->locD, p->n_obs,
+                                                                      p->n_state, n, root, p->dstatus);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_gram(p, false, p->locV, p->locD, nullptr, r, p->gram, s)) != cudaSuccess) return e;
+    if ((e = launch_levels(p, p->gram, p->A, nullptr, p->den, 0.0, s)) != cudaSuccess) return e;
+    if ((e = launch_rowgemm<1>(p, p->locV, p->A, p->locD, r, p->locZ, p->n_obs, s)) != cudaSuccess) return e;
+  }
+  if (p->n_state > 0) {
+    const size_t smem = localized_smem_bytes(n);
+    const unsigned grid = (unsigned)((p->n_state + LOC_TI - 1) / LOC_TI);
+    if (mode == 0) {
+      if ((e = cudaFuncSetAttribute(localized_update_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      localized_update_kernel<0><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, delta, idx, scale, XA,
+                                                                p->n_state, p->n_obs, n, root);
+    } else {
+      if ((e = cudaFuncSetAttribute(localized_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      localized_update_kernel<1><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, nullptr, idx, scale, XA,
+                                                                p->n_state, p->n_obs, n, root);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 int localized_common(enkf_plan* p, const double* X, const double* Y, const int64_t* idx, const double* r,
                      const double* delta, double scale, int mode, double* XA, void* stream, enkf_status* st) {
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
@@ -989,41 +1033,9 @@ int localized_common(enkf_plan* p, const double* X, const double* Y, const int64
     set_status(st, ENKF_INVALID_ARGUMENT, "influence scale must be positive");
     return ENKF_INVALID_ARGUMENT;
   }
-  const int n = p->n;
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t obs_elems = (size_t)p->n_obs * (size_t)n;
-  if (!p->locV && obs_elems) {
-    CUDA_TRY(cudaMalloc(&p->locV, sizeof(double) * obs_elems), st);
-    CUDA_TRY(cudaMalloc(&p->locD, sizeof(double) * obs_elems), st);
-    CUDA_TRY(cudaMalloc(&p->locZ, sizeof(double) * obs_elems), st);
-  }
-  const double root = std::sqrt((double)n - 1.0);
   CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
-  if (p->n_obs > 0) {
-    const int64_t threads = p->n_obs * 32;
-    obs_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(X, Y, idx, p->locV, p->locD, p->n_obs,
-                                                                      p->n_state, n, root, p->dstatus);
-    CUDA_TRY(cudaGetLastError(), st);
-    CUDA_TRY(launch_gram(p, false, p->locV, p->locD, nullptr, r, p->gram, s), st);
-    CUDA_TRY(launch_levels(p, p->gram, p->A, nullptr, p->den, 0.0, s), st);
-    CUDA_TRY(launch_rowgemm<1>(p, p->locV, p->A, p->locD, r, p->locZ, p->n_obs, s), st);
-  }
-  if (p->n_state > 0) {
-    const size_t smem = localized_smem_bytes(n);
-    const unsigned grid = (unsigned)((p->n_state + LOC_TI - 1) / LOC_TI);
-    if (mode == 0) {
-      CUDA_TRY(cudaFuncSetAttribute(localized_update_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem), st);
-      localized_update_kernel<0><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, delta, idx, scale, XA,
-                                                                p->n_state, p->n_obs, n, root);
-    } else {
-      CUDA_TRY(cudaFuncSetAttribute(localized_update_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem), st);
-      localized_update_kernel<1><<<grid, LOC_THREADS, smem, s>>>(X, p->locV, p->locZ, nullptr, idx, scale, XA,
-                                                                p->n_state, p->n_obs, n, root);
-    }
-    CUDA_TRY(cudaGetLastError(), st);
-  }
+  CUDA_TRY(launch_localized(p, X, Y, idx, r, delta, scale, mode, XA, s), st);
   return enkf_plan_sync_status(p, stream, st);
 }
 }  // namespace
@@ -1128,10 +1140,12 @@ int32_t enkf_inflate_f64(const double* X, double* Xout, int64_t n_rows, int64_t 
   return cudaGetLastError() == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
 }
 
-int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, const double* r,
-                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing, double inflation,
-                           double* mean_f, double* mean_a, void* stream, enkf_status* st,
-                           int32_t* failed_cycle) {
+namespace {
+// forecast -> (inflation) -> analysis cycles; loc_scale > 0: the analysis is localized
+// with the cyclic influence matrix of that scale (evaluated in-kernel)
+int cycle_l96(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, const double* r, int32_t n_cycles,
+              int32_t steps_per_cycle, double dt, double forcing, double inflation, double loc_scale,
+              double* mean_f, double* mean_a, void* stream, enkf_status* st, int32_t* failed_cycle) {
   if (failed_cycle) *failed_cycle = -1;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) {
@@ -1176,9 +1190,13 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
       inflate_kernel<<<mean_grid, 256, 0, s>>>(X, X, p->n_state, p->n, inflation);
       e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = launch_gram(p, true, X, Ys + (size_t)c * yelems, idx, r, p->gram, s);
-    if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);
-    if (e == cudaSuccess) e = launch_rowgemm<0>(p, X, p->T, nullptr, nullptr, X, p->n_state, s);
+    if (loc_scale > 0.0) {  // experiment.py:470-473 with localization=influence_matrix_cyclic(...)
+      if (e == cudaSuccess) e = launch_localized(p, X, Ys + (size_t)c * yelems, idx, r, nullptr, loc_scale, 1, X, s);
+    } else {
+      if (e == cudaSuccess) e = launch_gram(p, true, X, Ys + (size_t)c * yelems, idx, r, p->gram, s);
+      if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);
+      if (e == cudaSuccess) e = launch_rowgemm<0>(p, X, p->T, nullptr, nullptr, X, p->n_state, s);
+    }
     if (e == cudaSuccess && mean_a) {
       row_mean_kernel<<<mean_grid, 256, 0, s>>>(X, mean_a + (size_t)c * p->n_state, p->n_state, p->n);
       e = cudaGetLastError();
@@ -1198,6 +1216,28 @@ int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int6
   }
   set_status(st, ENKF_OK, "ok");
   return ENKF_OK;
+}
+}  // namespace
+
+int32_t enkf_cycle_l96_f64(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, const double* r,
+                           int32_t n_cycles, int32_t steps_per_cycle, double dt, double forcing, double inflation,
+                           double* mean_f, double* mean_a, void* stream, enkf_status* st,
+                           int32_t* failed_cycle) {
+  return cycle_l96(p, X, Ys, idx, r, n_cycles, steps_per_cycle, dt, forcing, inflation, 0.0, mean_f, mean_a,
+                   stream, st, failed_cycle);
+}
+
+int32_t enkf_cycle_l96_localized_f64(enkf_plan* p, double* X, const double* Ys, const int64_t* idx,
+                                     const double* r, int32_t n_cycles, int32_t steps_per_cycle, double dt,
+                                     double forcing, double inflation, double loc_scale, double* mean_f,
+                                     double* mean_a, void* stream, enkf_status* st, int32_t* failed_cycle) {
+  if (!(loc_scale > 0.0)) {
+    if (failed_cycle) *failed_cycle = -1;
+    set_status(st, ENKF_INVALID_ARGUMENT, "influence scale must be positive");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  return cycle_l96(p, X, Ys, idx, r, n_cycles, steps_per_cycle, dt, forcing, inflation, loc_scale, mean_f, mean_a,
+                   stream, st, failed_cycle);
 }
 
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the

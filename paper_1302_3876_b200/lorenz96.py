@@ -109,10 +109,12 @@ class CycleResult:
 
 
 def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per_cycle: int,
-              inflation: float = 1.0) -> CycleResult:
+              inflation: float = 1.0, localization_scale: float | None = None) -> CycleResult:
     """Closed-loop cycling on the device: for every cycle c, X <- forecast(X,
     steps_per_cycle RK4 steps); X <- inflate(X, inflation) when inflation > 1
-    (experiment.py:466-467); X <- analysis_step(X, perturbed[c], h, r).
+    (experiment.py:466-467); X <- analysis_step(X, perturbed[c], h, r), localized
+    with influence_matrix_cyclic(nstate, h, localization_scale) when a scale is
+    given (experiment.py:470-473; the taper is evaluated in-kernel).
 
     ``perturbed``: (cycles, nobs, nens) pre-staged perturbed observations
     (numpy or CUDA tensor).  Failures raise NumericalFailureError naming the
@@ -121,6 +123,8 @@ def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per
     cfg = model.config
     if inflation < 1.0:
         raise ValueError(f"inflation factor must be >= 1, got {inflation}")
+    if localization_scale is not None and not localization_scale > 0:
+        raise ValueError("influence scale must be positive")
     dev_in = _is_cuda_tensor(x0)
     device = torch.device("cuda", _cuda_ready(x0.device.index if dev_in else None))
     x = _f64_contig_device(x0, device).clone()
@@ -148,10 +152,16 @@ def cycle_l96(model: Lorenz96, x0, perturbed, h: SelectionOperator, r, steps_per
     st = _native.EnkfStatus()
     failed = ctypes.c_int32(-1)
     with plan.lock:
-        code = _native.lib().enkf_cycle_l96_f64(
-            plan.handle, x.data_ptr(), ys.data_ptr(), 0 if idx is None else idx.data_ptr(), rd.data_ptr(),
-            cycles, int(steps_per_cycle), cfg.dt, cfg.forcing, float(inflation), mean_f.data_ptr(), mean_a.data_ptr(),
-            _stream_ptr(device), ctypes.byref(st), ctypes.byref(failed))
+        if localization_scale is None:
+            code = _native.lib().enkf_cycle_l96_f64(
+                plan.handle, x.data_ptr(), ys.data_ptr(), 0 if idx is None else idx.data_ptr(), rd.data_ptr(),
+                cycles, int(steps_per_cycle), cfg.dt, cfg.forcing, float(inflation), mean_f.data_ptr(),
+                mean_a.data_ptr(), _stream_ptr(device), ctypes.byref(st), ctypes.byref(failed))
+        else:
+            code = _native.lib().enkf_cycle_l96_localized_f64(
+                plan.handle, x.data_ptr(), ys.data_ptr(), 0 if idx is None else idx.data_ptr(), rd.data_ptr(),
+                cycles, int(steps_per_cycle), cfg.dt, cfg.forcing, float(inflation), float(localization_scale),
+                mean_f.data_ptr(), mean_a.data_ptr(), _stream_ptr(device), ctypes.byref(st), ctypes.byref(failed))
     if code != _native.ENKF_OK:
         try:
             _native.raise_for_status(code, st, "enkf_cycle_l96_f64")

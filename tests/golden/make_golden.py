@@ -269,6 +269,34 @@ def lorenz96():
         x = ref_enkf.analysis_step(x, ob, h, r, "sherman")
         ma.append(x.mean(axis=1))
     out["cycinf_mean_f"], out["cycinf_mean_a"], out["cycinf_xa"] = np.stack(mf), np.stack(ma), x
+    # the lorenz-small preset's loop (presets/lorenz-small.ini: ns=40, N=20, R = I, analysis
+    # every 2 RK4 steps, inflation 1.05, cyclic localization scale 8), 8 cycles, with the
+    # identity H (pobs = 1) and with a stride-2 H
+    for tag, idxs in (("lcA", None), ("lcB", np.arange(0, 40, 2))):
+        ns, nens, cycles = 40, 20, 8
+        model = Lorenz96(Lorenz96Config(nstate=ns))
+        rng2 = make_rng(0xC3 if idxs is None else 0xC4)
+        truth = model.advance(8.0 + 0.01 * rng2.standard_normal(ns), 0.0, 500 * 0.05)
+        x = truth[:, None] + 0.4 * rng2.standard_normal((ns, nens))
+        h = ref_enkf.SelectionOperator.identity() if idxs is None else ref_enkf.SelectionOperator.from_indices(idxs)
+        nobs = ns if idxs is None else len(idxs)
+        r = np.ones(nobs)
+        delta = ref_enkf.influence_matrix_cyclic(ns, h, scale=8.0)
+        out[f"{tag}_x0"] = x
+        out[f"{tag}_idx"] = np.array([], dtype=np.int64) if idxs is None else np.asarray(idxs, dtype=np.int64)
+        ys, mf, ma = [], [], []
+        for c in range(cycles):
+            truth = model.advance(truth, 0.0, 0.1)
+            y = h.apply(truth) + rng2.standard_normal(nobs)
+            ob = perturb_observations(y, r, nens, rng2)
+            x = forecast_step(model, x, c * 0.1, (c + 1) * 0.1)
+            mf.append(x.mean(axis=1))
+            x = inflate(x, 1.05)
+            x = ref_enkf.analysis_step(x, ob, h, r, "sherman", localization=delta)
+            ma.append(x.mean(axis=1))
+            ys.append(ob.perturbed)
+        out[f"{tag}_r"], out[f"{tag}_ys"] = r, np.stack(ys)
+        out[f"{tag}_mean_f"], out[f"{tag}_mean_a"], out[f"{tag}_xa"] = np.stack(mf), np.stack(ma), x
     return out
 
 

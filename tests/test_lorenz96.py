@@ -55,6 +55,18 @@ def _inf_cases():
         i += 1
 
 
+@pytest.mark.parametrize("tag", ["lcA", "lcB"])
+def test_oracle_localized_loop_matches_reference(tag):
+    """The lorenz-small preset's loop (inflation 1.05, cyclic localization scale 8,
+    analysis every 2 RK4 steps) against the reference's own 8 cycles."""
+    g = load("lorenz96")
+    idx = g[f"{tag}_idx"] if g[f"{tag}_idx"].size else None
+    x, mf, ma = oracle.cycle_l96(g[f"{tag}_x0"], g[f"{tag}_ys"], idx, g[f"{tag}_r"], 2, inflation=1.05,
+                                 localization_scale=8.0)
+    assert rel_err(mf, g[f"{tag}_mean_f"]) <= 1e-12
+    assert rel_err(ma, g[f"{tag}_mean_a"]) <= 1e-12 and rel_err(x, g[f"{tag}_xa"]) <= 1e-12
+
+
 def test_oracle_inflate_and_inflated_loop_match_reference():
     for x, a, want in _inf_cases():
         assert np.array_equal(oracle.inflate(x, a), want)
@@ -140,6 +152,35 @@ def test_gpu_inflate_and_inflated_loop():
     assert rel_err(res.mean_f.cpu().numpy(), g["cycinf_mean_f"]) <= 1e-9
     assert rel_err(res.mean_a.cpu().numpy(), g["cycinf_mean_a"]) <= 1e-9
     assert rel_err(res.x.cpu().numpy(), g["cycinf_xa"]) <= 1e-9
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["lcA", "lcB"])
+def test_gpu_localized_loop_matches_reference(tag):
+    """The lorenz-small preset's loop on the device (enkf_cycle_l96_localized_f64:
+    forecast -> inflation 1.05 -> analysis localized with the in-kernel cyclic taper of
+    scale 8) against the reference's own 8 cycles, identity and stride-2 H."""
+    import torch
+    g = load("lorenz96")
+    idx = g[f"{tag}_idx"] if g[f"{tag}_idx"].size else None
+    h = P.SelectionOperator.identity() if idx is None else P.SelectionOperator.from_indices(idx)
+    model = P.Lorenz96(P.Lorenz96Config(nstate=g[f"{tag}_x0"].shape[0]))
+    res = P.cycle_l96(model, g[f"{tag}_x0"], g[f"{tag}_ys"], h, g[f"{tag}_r"], 2, inflation=1.05,
+                      localization_scale=8.0)
+    assert rel_err(res.mean_f.cpu().numpy(), g[f"{tag}_mean_f"]) <= 1e-9
+    assert rel_err(res.mean_a.cpu().numpy(), g[f"{tag}_mean_a"]) <= 1e-9
+    assert rel_err(res.x.cpu().numpy(), g[f"{tag}_xa"]) <= 1e-9
+    # the device loop equals per-cycle calls of the public localized analysis step
+    x = torch.from_numpy(g[f"{tag}_x0"]).cuda()
+    lazy = P.influence_matrix_cyclic(x.shape[0], h, scale=8.0)
+    for c in range(g[f"{tag}_ys"].shape[0]):
+        x = model.advance(x, 0.0, 0.1)
+        x = P.inflate(x, 1.05)
+        obs = P.ObservationBatch(y=None, perturbed=torch.from_numpy(g[f"{tag}_ys"][c]).cuda(), perturbations=None)
+        x = P.analysis_step(x, obs, h, g[f"{tag}_r"], "sherman", localization=lazy)
+    assert rel_err(res.x.cpu().numpy(), x.cpu().numpy()) <= 1e-13
+    with pytest.raises(ValueError):
+        P.cycle_l96(model, g[f"{tag}_x0"], g[f"{tag}_ys"], h, g[f"{tag}_r"], 2, localization_scale=0.0)
 
 
 @pytest.mark.gpu

@@ -15,6 +15,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import oracle  # noqa: E402  (CPU baseline: test/bench infrastructure)
 import paper_1302_3876_b200 as P  # noqa: E402
@@ -103,6 +104,32 @@ def time_cycled(cycles=100, cpu_cycles=5):
                                "cpu_threads": os.cpu_count(), "note": "wall clock incl. one sync per 100 cycles"}}
 
 
+def time_lorenz_small(cycles=200):
+    """The lorenz-small preset's assimilation loop (presets/lorenz-small.ini: 40 states,
+    20 members, all observed, R = I, analysis every 2 RK4 steps for 400 steps, inflation
+    1.05, cyclic localization scale 8) on the device (cycle_l96, localized) vs the CPU
+    oracle loop, on the golden fixture's first ensemble and staged observations."""
+    from golden_io import load
+    g = load("lorenz96")
+    x0, r = g["lcA_x0"], g["lcA_r"]
+    rng = np.random.Generator(np.random.Philox(0x51))
+    ys = x0.mean(axis=1)[None, :, None] + rng.standard_normal((cycles, x0.shape[0], x0.shape[1]))
+    model = P.Lorenz96(P.Lorenz96Config(nstate=x0.shape[0]))
+    h = P.SelectionOperator.identity()
+    P.cycle_l96(model, x0, ys[:2], h, r, 2, inflation=1.05, localization_scale=8.0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = P.cycle_l96(model, x0, ys, h, r, 2, inflation=1.05, localization_scale=8.0)
+    torch.cuda.synchronize()
+    gpu_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    xo, _, _ = oracle.cycle_l96(x0, ys, None, r, 2, inflation=1.05, localization_scale=8.0)
+    cpu_s = time.perf_counter() - t0
+    err = float(np.abs(res.x.cpu().numpy() - xo).max() / np.abs(xo).max())
+    return {"lorenz_small_loop": {"cycles": cycles, "gpu_s": gpu_s, "gpu_ms_per_cycle": gpu_s / cycles * 1e3,
+                                  "cpu_oracle_s": cpu_s, "cpu_threads": os.cpu_count(), "xa_rel_err_vs_oracle": err}}
+
+
 def time_localized(reps=5):
     """Localized analysis (enkf.py:193-199): GPU matrix-free cyclic
     influence (taper evaluated in-kernel), GPU with the dense influence matrix, and the
@@ -150,6 +177,7 @@ def main():
     out = {}
     if a.cycled:
         print(json.dumps(time_cycled()), flush=True)
+        print(json.dumps(time_lorenz_small()), flush=True)
     if a.localized:
         print(json.dumps(time_localized()), flush=True)
     for cfg in [int(c) for c in a.configs.split(",") if c]:
