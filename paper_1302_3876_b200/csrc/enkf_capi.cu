@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
@@ -40,6 +41,7 @@ struct enkf_plan {
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
+  bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
   bool g8_events = false;                 // measurement: events around the slice and MMA passes
   cudaEvent_t g8_ev[3] = {nullptr, nullptr, nullptr};
   unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
@@ -611,6 +613,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
     p->gram_fused = (strcmp(env, "i8fused") == 0);
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
+  if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
   if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
   if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
@@ -1000,6 +1003,34 @@ cudaError_t launch_localized(enkf_plan* p, const double* X, const double* Y, con
     if ((e = launch_gram(p, false, p->locV, p->locD, nullptr, r, p->gram, s)) != cudaSuccess) return e;
     if ((e = launch_levels(p, p->gram, p->A, nullptr, p->den, 0.0, s)) != cudaSuccess) return e;
     if ((e = launch_rowgemm<1>(p, p->locV, p->A, p->locD, r, p->locZ, p->n_obs, s)) != cudaSuccess) return e;
+  }
+  if (p->n_state > 0 && p->loc_dmma) {
+    auto run = [&](auto np_tag) -> cudaError_t {
+      constexpr int NPV = decltype(np_tag)::value;
+      const size_t smem = localized_dmma_smem_bytes(NPV);
+      const unsigned grid = (unsigned)((p->n_state + LD_TI - 1) / LD_TI);
+      cudaError_t err;
+      if (mode == 0) {
+        if ((err = cudaFuncSetAttribute(localized_update_dmma_kernel<NPV, 0>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+          return err;
+        localized_update_dmma_kernel<NPV, 0><<<grid, LD_THREADS, smem, s>>>(X, p->locV, p->locZ, delta, idx, scale,
+                                                                          XA, p->n_state, p->n_obs, n, root);
+      } else {
+        if ((err = cudaFuncSetAttribute(localized_update_dmma_kernel<NPV, 1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+          return err;
+        localized_update_dmma_kernel<NPV, 1><<<grid, LD_THREADS, smem, s>>>(X, p->locV, p->locZ, nullptr, idx,
+                                                                          scale, XA, p->n_state, p->n_obs, n, root);
+      }
+      return cudaGetLastError();
+    };
+    if (n <= 8) return run(std::integral_constant<int, 8>{});
+    if (n <= 16) return run(std::integral_constant<int, 16>{});
+    if (n <= 32) return run(std::integral_constant<int, 32>{});
+    if (n <= 64) return run(std::integral_constant<int, 64>{});
+    if (n <= 96) return run(std::integral_constant<int, 96>{});
+    return run(std::integral_constant<int, 128>{});
   }
   if (p->n_state > 0) {
     const size_t smem = localized_smem_bytes(n);
