@@ -167,3 +167,38 @@ def test_gpu_localized_device_resident_and_errors():
     bad[0, 0] = np.nan
     with pytest.raises(ValueError):
         P.analysis_step(c["x"], _obs(bad), h, c["r"], "sherman", localization=c["delta"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nens", [5, 20, 64, 100, 128])
+def test_gpu_localized_dmma_equals_cuda_core_form(nens, monkeypatch):
+    """The DMMA localized update (default) and the CUDA-core form (ENKF_LOCALIZED=fma)
+    agree to rounding on ragged sizes (state rows not a multiple of the 64-row CTA,
+    observation count not a multiple of the 32-row chunk, N not a multiple of 8)."""
+    import ctypes
+    import torch
+    from paper_1302_3876_b200 import _native
+    rng = make_rng(77 + nens)
+    ns, nobs = 1000, 333
+    x = rng.standard_normal((ns, nens)) + rng.standard_normal((ns, 1))
+    idx = np.sort(rng.choice(ns, size=nobs, replace=False)).astype(np.int64)
+    r = rng.uniform(0.25, 1.0, nobs)
+    pert = x[idx].mean(axis=1)[:, None] + rng.standard_normal((nobs, nens))
+    dev = torch.device("cuda", 0)
+    xd, yd, rd, idd = (torch.from_numpy(a).to(dev) for a in (x, pert, r, idx))
+    outs = {}
+    for mode in ("dmma", "fma"):
+        if mode == "fma":
+            monkeypatch.setenv("ENKF_LOCALIZED", "fma")
+        plan = _native.Plan(ns, nobs, nens, 0)
+        monkeypatch.delenv("ENKF_LOCALIZED", raising=False)
+        out = torch.empty_like(xd)
+        st = _native.EnkfStatus()
+        rc = _native.lib().enkf_analysis_localized_cyclic_f64(
+            plan.handle, xd.data_ptr(), yd.data_ptr(), idd.data_ptr(), rd.data_ptr(), 37.0, out.data_ptr(),
+            torch.cuda.current_stream().cuda_stream, ctypes.byref(st))
+        assert rc == 0, st.message
+        outs[mode] = out.cpu().numpy()
+    ref = oracle.analysis_step_localized(x, pert, idx, r, oracle.influence_matrix_cyclic(ns, idx, 37.0))
+    assert rel_err(outs["dmma"], outs["fma"]) <= 1e-13
+    assert rel_err(outs["dmma"], ref) <= 1e-11
