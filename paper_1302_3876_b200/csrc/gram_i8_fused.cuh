@@ -41,7 +41,7 @@ constexpr int GF_THREADS = (4 * GF_TEAMS + 7) * 32;
 constexpr int GF_NHB = 4;        // staging depth (half-blocks the loader runs ahead)
 constexpr int GF_XST = GF_HB * G8_N * 8;       // 16 KiB: X rows of a half-block
 constexpr int GF_STG = GF_XST + GF_HB * 8;     // + r of its rows
-constexpr long long GF_SPIN_LIMIT = 1ll << 31;  // ~minutes of polling: a deadlock traps instead
+constexpr long long GF_SPIN_LIMIT = 1ll << 24;  // ~10-20 s of polling: a deadlock traps instead of hanging
 
 __host__ __device__ inline size_t gram_i8_fused_smem_bytes() {
   return 1024 + (size_t)GF_NST * G8_STAGE + GF_NHB * (size_t)GF_STG + 2 * G8_N * 8 /*scales*/ +
