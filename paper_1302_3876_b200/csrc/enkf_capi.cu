@@ -20,6 +20,7 @@
 #include "gram_i8.cuh"
 #include "gram_i8_fused.cuh"
 #include "host_stream.cuh"
+#include "tiny.cuh"
 
 using namespace enkf;
 
@@ -42,6 +43,7 @@ struct enkf_plan {
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
+  bool tiny = true;                       // desk-scale problems: the whole step in one CTA (ENKF_TINY=0: off)
   bool g8_events = false;                 // measurement: events around the slice and MMA passes
   cudaEvent_t g8_ev[3] = {nullptr, nullptr, nullptr};
   unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
@@ -283,6 +285,17 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram128_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->partial, p->g128_cpb_vv, p->g128_cpb_vd, svv,
                                                                  svd, gram, overflow);
   }
+  return cudaGetLastError();
+}
+
+// Desk-scale analysis in one CTA (tiny.cuh); flags into p->dstatus.
+cudaError_t launch_tiny(const enkf_plan* p, const double* X, const double* Y, const int64_t* idx, const double* r,
+                        double* XA, cudaStream_t s) {
+  const size_t smem = (size_t)tiny_smem_doubles(p->n_obs, p->n) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(analysis_tiny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  analysis_tiny_kernel<<<1, TINY_THREADS, smem, s>>>(X, Y, idx, r, XA, p->n_state, p->n_obs, p->n,
+                                                     std::sqrt((double)(p->n - 1)), p->dstatus);
   return cudaGetLastError();
 }
 
@@ -614,6 +627,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
+  if (const char* env = getenv("ENKF_TINY")) p->tiny = (env[0] != '0');
   if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
   if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
@@ -731,6 +745,10 @@ int32_t enkf_analysis_async_f64(enkf_plan* p, const double* X, const double* Y, 
   if (p->n < 2) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s);
+  if (e == cudaSuccess && p->tiny && tiny_eligible(p->n_state, p->n_obs, p->n)) {
+    e = launch_tiny(p, X, Y, idx, r, XA, s);
+    return e == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
+  }
   if (e == cudaSuccess) e = launch_gram(p, true, X, Y, idx, r, p->gram, s);
   const double cscale = 1.0 / std::sqrt((double)(p->n - 1));
   if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);
@@ -1223,6 +1241,8 @@ int cycle_l96(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, con
     }
     if (loc_scale > 0.0) {  // experiment.py:470-473 with localization=influence_matrix_cyclic(...)
       if (e == cudaSuccess) e = launch_localized(p, X, Ys + (size_t)c * yelems, idx, r, nullptr, loc_scale, 1, X, s);
+    } else if (p->tiny && tiny_eligible(p->n_state, p->n_obs, p->n)) {
+      if (e == cudaSuccess) e = launch_tiny(p, X, Ys + (size_t)c * yelems, idx, r, X, s);
     } else {
       if (e == cudaSuccess) e = launch_gram(p, true, X, Ys + (size_t)c * yelems, idx, r, p->gram, s);
       if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);

@@ -243,12 +243,18 @@ def analysis_step(
     perturbed = obs.perturbed
     if not _is_cuda_tensor(perturbed):
         perturbed = np.asarray(perturbed, dtype=float)
-    r_host = r.detach().cpu().numpy() if _is_cuda_tensor(r) else np.asarray(r, dtype=float)
-    _check_obs_shapes(nobs, nens, tuple(perturbed.shape), r_host.shape)
-    if np.any(r_host <= 0):
-        raise ValueError("observation variances must be positive")
-    if not np.all(np.isfinite(r_host)):
-        raise ValueError("inputs contain non-finite entries")
+    if _is_cuda_tensor(r):
+        # device-resident r: its positivity / finiteness is checked by the Gram pass
+        # (FLAG_R_NONPOS / FLAG_NONFINITE -> the same ValueError), without a host copy
+        r_host = None
+        _check_obs_shapes(nobs, nens, tuple(perturbed.shape), tuple(r.shape))
+    else:
+        r_host = np.asarray(r, dtype=float)
+        _check_obs_shapes(nobs, nens, tuple(perturbed.shape), r_host.shape)
+        if np.any(r_host <= 0):
+            raise ValueError("observation variances must be positive")
+        if not np.all(np.isfinite(r_host)):
+            raise ValueError("inputs contain non-finite entries")
 
     if localization is not None:
         return _analysis_localized(x, perturbed, h, r, localization, nstate, nobs, nens, dev_in)
@@ -273,6 +279,8 @@ def analysis_step(
 
     device_index = _cuda_ready()
     plan = _native.get_plan(device_index, nstate, nobs, nens)
+    if r_host is None:  # host x with a device-resident r
+        r_host = r.detach().cpu().numpy()
     xh = np.ascontiguousarray(x, dtype=np.float64)
     yh = np.ascontiguousarray(perturbed, dtype=np.float64)
     rh = np.ascontiguousarray(r_host, dtype=np.float64)

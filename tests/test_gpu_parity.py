@@ -108,6 +108,24 @@ def test_device_flags_non_finite_and_nonpositive():
         P.solve_sherman(torch.tensor([1.0, 1.0, 0.0, 1.0], dtype=torch.float64, device=dev), v, torch.ones_like(v))
 
 
+@pytest.mark.parametrize("maker", ["config1", "config4s10"])
+def test_device_resident_r_validated_on_device(maker):
+    """A CUDA-tensor r is not copied back for validation: r <= 0 and non-finite r are
+    flagged by the Gram pass and raise the reference's ValueError (sherman.py:100-107)."""
+    import torch
+    p = {"config1": W.config1, "config4s10": lambda: W.config4(10)}[maker]()
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(p.x).to(dev)
+    obs = P.ObservationBatch(y=None, perturbed=torch.from_numpy(p.perturbed).to(dev), perturbations=None)
+    for bad in (0.0, -1.0, float("nan"), float("inf")):
+        r = torch.from_numpy(p.r).to(dev)
+        r[len(p.r) // 2] = bad
+        with pytest.raises(ValueError):
+            P.analysis_step(x, obs, h_of(p), r)
+    xa = P.analysis_step(x, obs, h_of(p), torch.from_numpy(p.r).to(dev))
+    assert rel_err(xa.cpu().numpy(), oracle.analysis_step(p.x, p.perturbed, p.indices, p.r)) <= XA_TOL
+
+
 def _levels_on(gram_host, n):
     import torch
     dev = torch.device("cuda", 0)
@@ -528,3 +546,47 @@ def test_tensor_core_anomaly_extreme_rows():
         rowscale = np.abs(want[lo:hi]).max(axis=1, keepdims=True)
         assert np.all(np.isfinite(got[lo:hi]))
         assert (np.abs(got[lo:hi] - want[lo:hi]) / rowscale).max() <= tol, (lo, hi)
+
+
+@pytest.mark.parametrize("n,nobs,ns", [(2, 3, 5), (5, 17, 40), (20, 20, 40), (33, 100, 300), (64, 512, 1024),
+                                       (20, 40, 40)])
+def test_tiny_path_equals_multi_kernel_path(n, nobs, ns, monkeypatch):
+    """Desk-scale problems take the one-CTA kernel (tiny.cuh); it agrees with the
+    multi-kernel path (ENKF_TINY=0) to rounding, in place (XA = X) and out of place,
+    and keeps the index / validation errors."""
+    import torch
+    dev = torch.device("cuda", 0)
+    g = np.random.Generator(np.random.Philox(500 + n + nobs))
+    x = g.standard_normal((ns, 1)) + g.uniform(0.3, 2.0) * g.standard_normal((ns, n))
+    idx = None if nobs == ns else np.sort(g.choice(ns, nobs, replace=False)).astype(np.int64)
+    r = g.uniform(0.2, 1.5, nobs)
+    y = (x if idx is None else x[idx]).mean(axis=1, keepdims=True) + g.standard_normal((nobs, n))
+    xd, yd, rd = (torch.from_numpy(a).to(dev) for a in (x, y, r))
+    idd = None if idx is None else torch.from_numpy(idx).to(dev)
+    s = torch.cuda.current_stream().cuda_stream
+
+    def run(tiny, inplace=False):
+        monkeypatch.setenv("ENKF_TINY", "1" if tiny else "0")
+        plan = _native.Plan(ns, nobs, n, 0)
+        monkeypatch.delenv("ENKF_TINY")
+        xin = xd.clone()
+        out = xin if inplace else torch.empty_like(xd)
+        st = _native.EnkfStatus()
+        rc = _native.lib().enkf_analysis_f64(plan.handle, xin.data_ptr(), yd.data_ptr(),
+                                            0 if idd is None else idd.data_ptr(), rd.data_ptr(), out.data_ptr(), s,
+                                            ctypes.byref(st))
+        assert rc == 0, st.message
+        return out.cpu().numpy()
+
+    a, b, c = run(True), run(False), run(True, inplace=True)
+    assert rel_err(a, b) <= 1e-13
+    assert np.array_equal(a, c)
+    assert rel_err(a, oracle.analysis_step(x, y, idx, r)) <= XA_TOL
+    if idx is not None and nobs > 2:  # the index checks of the Gram pass hold in the tiny kernel
+        bad = idd.clone()
+        bad[1] = bad[0]
+        plan = _native.Plan(ns, nobs, n, 0)
+        st = _native.EnkfStatus()
+        rc = _native.lib().enkf_analysis_f64(plan.handle, xd.data_ptr(), yd.data_ptr(), bad.data_ptr(),
+                                            rd.data_ptr(), torch.empty_like(xd).data_ptr(), s, ctypes.byref(st))
+        assert rc == _native.ENKF_INVALID_ARGUMENT
