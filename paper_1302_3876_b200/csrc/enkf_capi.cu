@@ -44,6 +44,8 @@ struct enkf_plan {
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
   bool tiny = true;                       // desk-scale problems: the whole step in one CTA (ENKF_TINY=0: off)
+  char* small_h = nullptr;                // host path for small problems: page-locked staging block
+  char* small_d = nullptr;                // and its device twin
   bool g8_events = false;                 // measurement: events around the slice and MMA passes
   cudaEvent_t g8_ev[3] = {nullptr, nullptr, nullptr};
   unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
@@ -93,6 +95,7 @@ struct enkf_plan {
 namespace {
 
 const char* kVersion = "enkf_b200 0.1.0 sm_100a";
+constexpr size_t kSmallHostBytes = (size_t)1 << 20;  // small-problem host path: all inputs <= 1 MiB
 
 void set_status(enkf_status* st, int code, const char* fmt, ...) {
   if (!st) return;
@@ -691,6 +694,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->hidx);
   if (p->hstream) cudaStreamDestroy(p->hstream);
   cudaFree(p->hxo);
+  if (p->small_h) cudaFreeHost(p->small_h);
+  cudaFree(p->small_d);
   if (p->hs_in) cudaStreamDestroy(p->hs_in);
   if (p->hs_out) cudaStreamDestroy(p->hs_out);
   if (p->ev_obs) cudaEventDestroy(p->ev_obs);
@@ -933,6 +938,44 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     CUDA_TRY(cudaMalloc(&p->hidx, sizeof(int64_t) * (size_t)p->n_obs + 16), st);
   }
   cudaStream_t s = p->hstream;
+  {
+    // Small problems: every input packed into one page-locked staging block, one
+    // copy in, the step (in place), X^A and the status out, one synchronisation.
+    const size_t xb = sizeof(double) * (size_t)p->n_state * n, yb = sizeof(double) * (size_t)p->n_obs * n;
+    const size_t rb = sizeof(double) * (size_t)p->n_obs, ib = idx_h ? sizeof(int64_t) * (size_t)p->n_obs : 0;
+    auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+    const size_t total = al(xb) + al(yb) + al(rb) + al(ib);
+    if (total <= kSmallHostBytes) {
+      if (!p->small_h) {
+        CUDA_TRY(cudaMallocHost(&p->small_h, kSmallHostBytes), st);
+        CUDA_TRY(cudaMalloc(&p->small_d, kSmallHostBytes), st);
+      }
+      char* h = p->small_h;
+      char* d = p->small_d;
+      memcpy(h, X_h, xb);
+      memcpy(h + al(xb), Y_h, yb);
+      memcpy(h + al(xb) + al(yb), r_h, rb);
+      if (ib) memcpy(h + al(xb) + al(yb) + al(rb), idx_h, ib);
+      CUDA_TRY(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s), st);
+      double* dx = reinterpret_cast<double*>(d);
+      const double* dy = reinterpret_cast<const double*>(d + al(xb));
+      const double* dr = reinterpret_cast<const double*>(d + al(xb) + al(yb));
+      const int64_t* di = ib ? reinterpret_cast<const int64_t*>(d + al(xb) + al(yb) + al(rb)) : nullptr;
+      int rc = enkf_analysis_async_f64(p, dx, dy, di, dr, dx, s);  // in place
+      if (rc != ENKF_OK) {
+        cudaStreamSynchronize(s);
+        CUDA_TRY(cudaGetLastError(), st);
+        set_status(st, rc, "launch failed");
+        return rc;
+      }
+      CUDA_TRY(cudaMemcpyAsync(h, dx, xb, cudaMemcpyDeviceToHost, s), st);
+      CUDA_TRY(cudaMemcpyAsync(p->hstatus, p->dstatus, sizeof(DevStatus), cudaMemcpyDeviceToHost, s), st);
+      CUDA_TRY(cudaStreamSynchronize(s), st);
+      const int rc2 = translate_status(p, st);
+      if (rc2 == ENKF_OK) memcpy(XA_h, h, xb);
+      return rc2;
+    }
+  }
   if (idx_h && p->n_obs > 0 && p->host_streamed) {
     const void* Xmap = mapped_device_ptr(X_h);
     if (Xmap && is_pinned(XA_h))
