@@ -308,7 +308,7 @@ cudaError_t launch_levels(const enkf_plan* p, const double* gram, double* A, dou
     const size_t smem = (size_t)levels_blk_smem_doubles(p->n) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(ism_levels_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    ism_levels_blocked_kernel<<<1, 1024, smem, s>>>(gram, p->n, cscale, A, T, den, p->dstatus);
+    ism_levels_blocked_kernel<<<1, LV_THREADS, smem, s>>>(gram, p->n, cscale, A, T, den, p->dstatus);
     return cudaGetLastError();
   }
   const size_t smem = (size_t)levels_smem_doubles(p->n) * sizeof(double);
@@ -1334,6 +1334,10 @@ int32_t enkf_cycle_l96_localized_f64(enkf_plan* p, double* X, const double* Ys, 
                    stream, st, failed_cycle);
 }
 
+// Profiling-only: per-block phase clocks of the blocked levels kernel (-DLV_TRACE_ON)
+__attribute__((visibility("default"))) int32_t enkf_debug_lv_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, enkf::g_lv_trace, sizeof(enkf::g_lv_trace)) == cudaSuccess ? 0 : 5;
+}
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {

@@ -1124,13 +1124,23 @@ ism_levels_kernel(const double* __restrict__ gram, int n, double cscale,
 // V'V (packed, smem) and of V'D (registers).  4 barriers per block instead of
 // 1 per level.
 constexpr int LB = 8;
+// profiling only (-DLV_TRACE_ON): clock64 stamps of thread 0 per block and phase
+__device__ long long g_lv_trace[20][6];
+#ifdef LV_TRACE_ON
+#define LV_TRACE(blk, ph) do { if (threadIdx.x == 0) g_lv_trace[(blk)][(ph)] = clock64(); } while (0)
+#else
+#define LV_TRACE(blk, ph) do { } while (0)
+#endif
+#ifndef LV_THREADS
+#define LV_THREADS 512  // 128 registers per thread: the 1024-thread form spilled (ncu: STL in the trailing update)
+#endif
 
 __host__ __device__ inline int64_t levels_blk_smem_doubles(int n) {
   return levels_vv_doubles(n) + (int64_t)n * n /*VD*/ + (int64_t)LB * n /*PT*/ +
          (int64_t)LB * 2 * n /*R/Q*/ + (int64_t)LB * LB /*L*/ + 2 * LB /*D, 1/D*/ + n /*colmean*/ + 16;
 }
 
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(LV_THREADS, 1)
 ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
                           double* __restrict__ A, double* __restrict__ T,
                           double* __restrict__ den_out, DevStatus* __restrict__ status) {
@@ -1151,22 +1161,50 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
   for (int e = tid; e < n * n; e += nthr) {
     const int i = e / n, c = e - i * n;
     if (i <= c) vv[P(i, c)] = gram[(int64_t)i * n2 + c];
-    vd[e] = gram[(int64_t)i * n2 + n + c];
   }
+  // V'D lives in DMMA accumulator fragments: warp w owns the 32 x 32 tile (rows
+  // 32(w&3).., cols 32(w>>2)..), 4 x 4 m8n8 tiles; lane holds (row fr, cols 2fk, 2fk+1)
+  static_assert(LV_THREADS == 512, "the V'D register tiling assumes 16 warps");
+  const int wm = warp & 3, wn = warp >> 2, fr = lane >> 2, fk = lane & 3;
+  double vdr[4][4][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 32 * wm + 8 * mt + fr, c = 32 * wn + 8 * nt + 2 * fk + e;
+        vdr[mt][nt][e] = (i < n && c < n) ? gram[(int64_t)i * n2 + n + c] : 0.0;
+      }
   if (tid == 0) *fail = 0;
   __syncthreads();
 
   for (int k0 = 0; k0 < n; k0 += LB) {
     const int b = (n - k0) < LB ? (n - k0) : LB;
     const int c0 = k0 + b;  // first trailing V'V column
+    LV_TRACE(k0 / LB, 0);
     // ---- 1. gather P = Gamma[:, K], R = Gamma[K, trailing] (M = I + Gamma[K, K] is in PT)
     for (int e = tid; e < b * n; e += nthr) {
       const int j = e / n, i = e - j * n, k = k0 + j;
       PT[j * n + i] = (i <= k) ? vv[P(i, k)] : vv[P(k, i)];
       if (i >= c0) RQ[j * n2 + i] = vv[P(k, i)];
-      RQ[j * n2 + n + i] = vd[k * n + i];
+    }
+    // the block's V'D rows k0..k0+b-1 (R, V'D part) straight from the owning fragments
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = 32 * wm + 8 * mt + fr;
+      if (i >= k0 && i < k0 + b) {
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = 32 * wn + 8 * nt + 2 * fk + e;
+            if (c < n) RQ[(i - k0) * n2 + n + c] = vdr[mt][nt][e];
+          }
+      }
     }
     __syncthreads();
+    LV_TRACE(k0 / LB, 1);
     // ---- 2. LDL' of M = I + Gamma[K, K] (the block's den_k), one warp in
     //         registers: lane l holds entries l and l+32 of the row-major 8x8
     //         block; column j is broadcast by shuffles at step j.  Dm = den,
@@ -1223,6 +1261,7 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
     }
     __syncthreads();
     if (*fail) return;  // uniform
+    LV_TRACE(k0 / LB, 2);
     // ---- 3. Q = M^-1 R, one trailing column per thread
     const int nv = n - c0;  // trailing V'V columns
     for (int t = tid; t < nv + n; t += nthr) {
@@ -1245,6 +1284,7 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
         if (j < b) RQ[j * n2 + col] = y[j];
     }
     __syncthreads();
+    LV_TRACE(k0 / LB, 3);
     // ---- 4. rank-b update of the trailing V'V (warp per column) and all of V'D
 #pragma unroll 1
     for (int c = c0 + warp; c < n; c += nwarps) {
@@ -1260,39 +1300,41 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
         col[i] = acc;
       }
     }
-    // V'D: 4 x 4 register tiles, P and Q loaded once per tile (rows 4w.., cols 4l..)
-#pragma unroll 1
-    for (int tile = tid; tile < ((n + 3) >> 2) * ((n + 3) >> 2); tile += nthr) {
-      const int nt = (n + 3) >> 2;
-      const int i0 = 4 * (tile / nt), c0v = 4 * (tile - (tile / nt) * nt);
-      double acc[4][4];
+    // V'D -= P Q on the FP64 tensor pipe (DMMA m8n8k4, two k-steps of the rank-b
+    // update; A = -P from PT, B = Q from RQ, zero beyond b and n)
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+    for (int ks = 0; ks < LB / 4; ++ks) {
+      const int j = 4 * ks + fk;
+      double a[4], bq[4];
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
-          acc[a][bb] = (i0 + a < n && c0v + bb < n) ? vd[(i0 + a) * n + c0v + bb] : 0.0;
-#pragma unroll
-      for (int j = 0; j < LB; ++j) {
-        if (j >= b) break;
-        double pv[4], qv[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) pv[a] = (i0 + a < n) ? PT[j * n + i0 + a] : 0.0;
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb) qv[bb] = (c0v + bb < n) ? RQ[j * n2 + n + c0v + bb] : 0.0;
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int bb = 0; bb < 4; ++bb) acc[a][bb] -= pv[a] * qv[bb];
+      for (int mt = 0; mt < 4; ++mt) {
+        const int i = 32 * wm + 8 * mt + fr;
+        a[mt] = (j < b && i < n) ? -PT[j * n + i] : 0.0;
       }
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
+      for (int nt = 0; nt < 4; ++nt) {
+        const int c = 32 * wn + 8 * nt + fr;
+        bq[nt] = (j < b && c < n) ? RQ[j * n2 + n + c] : 0.0;
+      }
 #pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
-          if (i0 + a < n && c0v + bb < n) vd[(i0 + a) * n + c0v + bb] = acc[a][bb];
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma884(vdr[mt][nt][0], vdr[mt][nt][1], a[mt], bq[nt]);
     }
     __syncthreads();
   }
 
+  LV_TRACE(16, 0);
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int i = 32 * wm + 8 * mt + fr, c = 32 * wn + 8 * nt + 2 * fk + e;
+        if (i < n && c < n) vd[i * n + c] = vdr[mt][nt][e];
+      }
+  __syncthreads();
   // A = V'Z; T = I + cscale (A - 1 colmean(A)')
   for (int e = tid; e < n * n; e += nthr) A[e] = vd[e];
   if (T != nullptr) {
