@@ -1131,6 +1131,9 @@ __device__ long long g_lv_trace[20][6];
 #else
 #define LV_TRACE(blk, ph) do { } while (0)
 #endif
+#ifndef LV_SERIAL_LDL
+#define LV_SERIAL_LDL 1  // pivot-block LDL' by one thread in registers (0: the warp-shuffle form)
+#endif
 #ifndef LV_THREADS
 #define LV_THREADS 512  // 128 registers per thread: the 1024-thread form spilled (ncu: STL in the trailing update)
 #endif
@@ -1209,6 +1212,43 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
     //         registers: lane l holds entries l and l+32 of the row-major 8x8
     //         block; column j is broadcast by shuffles at step j.  Dm = den,
     //         Dm[LB + j] = 1/den (one reciprocal per pivot), Lm unit lower.
+#if LV_SERIAL_LDL
+    // one thread, the whole b x b block in registers (the shuffle-based warp form
+    // spent ~4K cycles per block in dependent shuffle rounds)
+    if (tid == 0) {
+      double m[LB][LB];
+#pragma unroll
+      for (int r = 0; r < LB; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c)
+          m[r][c] = (r < b && c < b) ? (r == c ? 1.0 : 0.0) + PT[c * n + k0 + r] : 0.0;
+      bool sing = false;
+#pragma unroll
+      for (int jj = 0; jj < LB; ++jj) {
+        if (jj >= b || sing) break;
+        const double d = m[jj][jj];
+        if (fabs(d) < kSingularTol) {
+          if (!(atomicOr(&status->flags, FLAG_SINGULAR) & FLAG_SINGULAR)) {
+            status->level = k0 + jj + 1;
+            status->den = d;
+          }
+          *fail = 1;
+          sing = true;
+          break;
+        }
+        const double dinv = 1.0 / d;
+        Dm[jj] = d;
+        Dm[LB + jj] = dinv;
+        if (den_out) den_out[k0 + jj] = d;
+#pragma unroll
+        for (int r = jj + 1; r < LB; ++r) {
+          if (r < b) Lm[r * LB + jj] = m[r][jj] * dinv;
+#pragma unroll
+          for (int c = jj + 1; c <= r; ++c) m[r][c] -= m[r][jj] * m[c][jj] * dinv;
+        }
+      }
+    }
+#else
     if (warp == 0) {
       double m[2];
       int er[2], ec[2];
@@ -1259,6 +1299,7 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
         }
       }
     }
+#endif
     __syncthreads();
     if (*fail) return;  // uniform
     LV_TRACE(k0 / LB, 2);
