@@ -53,6 +53,8 @@ def main():
             lib.enkf_anomaly_update_f64(plan.handle, x.data_ptr(), t.data_ptr(), xa.data_ptr(), ns, s)
 
         stages = [("gram_" + mode, gram_once)] + ([("anomaly", anomaly_once)] if mode == "i8" else [])
+        if mode == "i8" and dbg is None:
+            stages.append(("plain_copy_X_to_XA", lambda: xa.copy_(x)))
         if dbg is not None:
             stages = [("anomaly_dbg" + dbg, anomaly_once)]
         for name, fn in stages:
