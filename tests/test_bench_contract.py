@@ -1,0 +1,46 @@
+"""bench.py keeps the driver's JSON contract (one line on rank 0 with the base keys,
+roofline, cpu_baseline, e2e, clocks, gpu_launches) on a shrunk config-5 workload,
+and the reference arm prints its line; the CPU part runs everywhere."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, timeout=900):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                         timeout=timeout, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--scale-log2", "6"])
+    assert BASE_KEYS <= set(d) and d["impl"] == "reference"
+    assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["value"] > 0 and d["higher_is_better"] is True
+
+
+@pytest.mark.gpu
+def test_bench_line_contract():
+    d = _run(["--steps", "3", "--warmup", "3", "--scale-log2", "6", "--e2e-steps", "1"])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] < 1.2 and r["peak"] > 0 and r["unit"] in ("GB/s", "TFLOP/s")
+    assert d["cpu_baseline"]["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    assert d["gpu_launches"] > 0
+    assert d["ism_sweep"] is None or 0 < d["ism_sweep"]["frac"] < 1.2
