@@ -1,5 +1,6 @@
 // enkf_capi.cu — the C ABI (include/enkf_b200.h) over the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -96,6 +97,13 @@ namespace {
 
 const char* kVersion = "enkf_b200 0.1.0 sm_100a";
 constexpr size_t kSmallHostBytes = (size_t)1 << 20;  // small-problem host path: all inputs <= 1 MiB
+
+// NVTX range for the host-side phases (visible in Nsight Systems; header-only, no
+// library dependency, no cost without a profiler attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 void set_status(enkf_status* st, int code, const char* fmt, ...) {
   if (!st) return;
@@ -746,6 +754,7 @@ int32_t enkf_anomaly_update_f64(enkf_plan* p, const double* X, const double* T, 
 
 int32_t enkf_analysis_async_f64(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
                                 const double* r, double* XA, void* stream) {
+  NvtxRange nvtx("enkf_analysis");
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -850,6 +859,7 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
     if (p->host_trace) cudaEventRecord(tr[i], ms);
   };
   // 1. observation side
+  NvtxRange nvtx1("host_streamed: observation side + Gram + levels");
   mark(0, s);
   CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
   CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
@@ -924,6 +934,7 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
 int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_h,
                                const int64_t* idx_h, const double* r_h, double* XA_h,
                                enkf_status* st) {
+  NvtxRange nvtx("enkf_analysis_host");
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) {
     set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
@@ -1011,6 +1022,7 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
 
 int32_t enkf_ism_solve_f64(enkf_plan* p, const double* r, const double* V, const double* D,
                            double* Z, double* A, void* stream, enkf_status* st) {
+  NvtxRange nvtx("enkf_ism_solve");
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
