@@ -266,7 +266,8 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
       return e;
-    const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * 3);
+    // 2 CTAs per SM are resident (120 registers x 256 threads): one full wave, no tail
+    const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * G8_SLICE_CTAS_PER_SM);
     gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
                                                                          p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                          p->dstatus);

@@ -65,6 +65,9 @@ __host__ __device__ inline int64_t g8_sample_stride(int64_t n_obs) {
 }
 constexpr int G8_HEADROOM = 2;   // scale exponent headroom (bits) over the sampled max
 constexpr int G8_SLICE_THREADS = 256;
+#ifndef G8_SLICE_CTAS_PER_SM
+#define G8_SLICE_CTAS_PER_SM 2   // the resident count: a grid of one full wave
+#endif
 constexpr int G8_VLD = 2 * G8_N + 1;  // slice-kernel staging row stride (uint64)
 
 __host__ __device__ inline size_t gram_i8_smem_bytes() {
