@@ -202,6 +202,10 @@ def _host_result(shape) -> np.ndarray:
 
 
 def _check_obs_shapes(nobs: int, nens: int, perturbed_shape, r_shape):
+    if nobs == 0:
+        # the reference fails on an empty observation set too: ValueError from the
+        # first rank-1 update of its empty panel (sherman.py:187)
+        raise ValueError("the Sherman-Morrison sweep needs at least one observation")
     if len(perturbed_shape) != 2 or tuple(perturbed_shape) != (nobs, nens):
         raise ValueError(f"perturbed observations have shape {tuple(perturbed_shape)}, "
                          f"expected ({nobs}, {nens})")

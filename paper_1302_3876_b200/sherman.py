@@ -92,6 +92,8 @@ def _validate_host(r, v, d):
         raise ValueError(f"column mismatch: V has {v.shape[1]}, D has {d.shape[1]}")
     if v.shape[1] < 1:
         raise ValueError("need at least one ensemble column")
+    if v.shape[0] < 1:  # the reference's sweep raises ValueError on an empty panel (sherman.py:187)
+        raise ValueError("the Sherman-Morrison sweep needs at least one observation")
     if np.any(r <= 0):
         raise ValueError("observation variances must be positive")
     if not (np.all(np.isfinite(v)) and np.all(np.isfinite(d)) and np.all(np.isfinite(r))):
@@ -110,6 +112,8 @@ def _validate_shapes_device(r, v, d):
         raise ValueError("column mismatch between V and D")
     if v.shape[1] < 1:
         raise ValueError("need at least one ensemble column")
+    if v.shape[0] < 1:  # the reference's sweep raises ValueError on an empty panel (sherman.py:187)
+        raise ValueError("the Sherman-Morrison sweep needs at least one observation")
 
 
 def _solve_device(r, v, d, return_a: bool = False):

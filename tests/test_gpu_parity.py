@@ -94,6 +94,9 @@ def test_validation_errors():
     bad[0, 0] = np.inf
     with pytest.raises(ValueError):
         P.solve_sherman(np.array([1.0, 1.0]), bad, np.ones((2, 2)))
+    # empty observation set: the reference's sweep raises ValueError (sherman.py:187)
+    with pytest.raises(ValueError):
+        P.solve_sherman(np.zeros(0), np.zeros((0, 3)), np.zeros((0, 3)))
 
 
 def test_device_flags_non_finite_and_nonpositive():

@@ -87,6 +87,11 @@ def test_analysis_step_argument_errors_before_device():
                         localization=P.influence_matrix_cyclic(7, P.SelectionOperator.identity()))
     with pytest.raises(ValueError):
         P.analysis_step(np.ones((6, 4)), obs, h, np.ones(2), solver="nope")
+    # an empty observation set (identity H on zero states): the reference raises
+    # ValueError from its sweep's first rank-1 update (sherman.py:187)
+    empty = P.ObservationBatch(y=np.zeros(0), perturbed=np.zeros((0, 4)), perturbations=np.zeros((0, 4)))
+    with pytest.raises(ValueError):
+        P.analysis_step(np.ones((0, 4)), empty, P.SelectionOperator.identity(), np.ones(0))
 
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
