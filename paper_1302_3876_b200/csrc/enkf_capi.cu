@@ -194,8 +194,8 @@ cudaError_t launch_gram(enkf_plan* p, bool analysis, const double* X, const doub
       gram128_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, p->g128_cpb_vv,
                                                                      p->g128_cpb_vd, svv, svd, gram, nullptr);
     else
-      gram_ws_reduce<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
-                                                                    svv, svd, gram);
+      gram_ws_reduce<<<(unsigned)((count + 31) / 32), 32 * GWR_SPLIT, 0, s>>>(p->partial, n, p->ws_ctas_per_block,
+                                                                            svv, svd, gram);
     return cudaGetLastError();
   }
   const bool vec = (n % 2 == 0) && aligned16(X) && aligned16(Y);
