@@ -5,6 +5,7 @@
 set -u
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q > gpurun_out/cap_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/cap_tests.log
+python -m pytest tests/test_fullsize_gpu.py -m gpu -q -s 2>&1 | grep -a "full-size parity" > gpurun_out/cap_fullsize.txt
 python bench.py > gpurun_out/cap_bench.json 2> gpurun_out/cap_bench.err; echo "bench rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cap_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/cap_ncu_bench.log 2>&1; echo "ncu list rc=$?"
