@@ -43,6 +43,8 @@ struct enkf_plan {
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
+  bool gram_ls = false;                   // level-split N = 256 MMA pass (opt-in: ENKF_GRAM=i8ls)
+  double* g8_ls_partial = nullptr;        // [groups][4][256][128] (level-split form)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
   bool tiny = true;                       // desk-scale problems: the whole step in one CTA (ENKF_TINY=0: off)
   char* small_h = nullptr;                // host path for small problems: page-locked staging block
@@ -272,7 +274,17 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
                                                                          p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                          p->dstatus);
   if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
-  {
+  if (p->gram_ls) {
+    if (!p->g8_ls_partial &&
+        (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
+      return e;
+    const size_t smem = gram_i8_ls_smem_bytes();
+    if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
+                                                                       p->g8_ls_partial, overflow);
+  } else {
     const size_t smem = gram_i8_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
@@ -283,7 +295,11 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
-  gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
+  if (p->gram_ls && !p->gram_fused)
+    gram_i8_ls_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_ls_partial, p->g8_groups, svv, svd, overflow,
+                                                                    gram);
+  else
+    gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
   // FP64 fallback, a no-op unless an element fell outside the sampled scales
   {
     const int ld = padded_ld(W_TILE);
@@ -636,6 +652,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
     p->gram_fused = (strcmp(env, "i8fused") == 0);
+    p->gram_ls = (strcmp(env, "i8ls") == 0);
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
@@ -721,6 +738,7 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->g8_flags);
   cudaFree(p->g8_meta);
   cudaFree(p->g8_partial);
+  cudaFree(p->g8_ls_partial);
   cudaFree(p->cyc_status);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);

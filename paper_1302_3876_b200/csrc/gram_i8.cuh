@@ -638,6 +638,177 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
   }
 }
 
+// ---------------------------------------------------------------------------
+// Level-split MMA pass (opt-in, ENKF_GRAM=i8ls).  The 4 CTAs of a group split the
+// digit pairs by level l = p + q instead of by output column: CTA r owns the level
+// set G8LS_SETS[r] ({7}, {8, 2}, {6, 3}, {5, 4}: 6, 6, 7, 7 pairs) for all 256
+// output columns [P'P | P'Q], in two 256-column int32 accumulators (all of TMEM).
+// Each pair is ONE N = 256 MMA with A = P_p and B = [P_q ; Q_q] straight from
+// shared memory (the producer lays each block's planes out as P_1 Q_1 P_2 Q_2 ...,
+// so one 256-row K-major descriptor spans P_q and Q_q): no tcgen05.cp, 4x the math
+// per instruction of the column split (tools/probe/g8_levelsplit_probe.cu: N = 256
+// from shared memory runs at the 128-cycle math floor).  The flush folds the CTA's
+// two levels into its fp64 partial [group][r][256 columns][128 members]
+// (read-modify-write in global memory, coalesced across a warp's members);
+// gram_i8_ls_reduce sums groups and level sets in a fixed order.
+constexpr int G8LS_NST = 4;                        // 48 KiB stages
+constexpr int G8LS_STAGE = 2 * G8_ND * G8_PLANE;   // P_1 Q_1 ... P_6 Q_6
+constexpr int G8LS_THREADS = 6 * 32;
+__host__ __device__ constexpr size_t gram_i8_ls_smem_bytes() {
+  return (size_t)G8LS_NST * G8LS_STAGE + (2 * G8LS_NST + 2) * 8 + 16 + 1024;
+}
+__device__ __forceinline__ uint32_t idesc_g8_n256() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+// level set of CTA r: first and second level (p + q), 0 = none
+__device__ __forceinline__ int g8ls_level(int r, int k) {
+  const int a[4] = {7, 8, 6, 5}, b[4] = {0, 2, 3, 4};
+  return k == 0 ? a[r] : b[r];
+}
+
+__global__ void __launch_bounds__(G8LS_THREADS, 1)
+gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned long long* __restrict__ cmax,
+                      int64_t n_blocks, int64_t blocks_per_group, double* __restrict__ partial,
+                      const int* __restrict__ overflow) {
+  if (*overflow) return;  // the FP64 fallback computes the Gram
+  extern __shared__ __align__(1024) unsigned char g8sm_raw[];
+  unsigned char* sm = g8sm_raw + ((1024u - (smem_u32(g8sm_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + G8LS_NST * G8LS_STAGE);
+  uint64_t* sfull = bars;
+  uint64_t* sempty = bars + G8LS_NST;
+  uint64_t* afull = bars + 2 * G8LS_NST;
+  uint64_t* aempty = afull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = blockIdx.x & 3;
+  const int64_t grp = blockIdx.x >> 2;
+  const int64_t b0 = grp * blocks_per_group;
+  const int64_t b1 = b0 + blocks_per_group < n_blocks ? b0 + blocks_per_group : n_blocks;
+  const int64_t nblk = b1 > b0 ? b1 - b0 : 0;
+  const int lv0 = g8ls_level(r, 0), lv1 = g8ls_level(r, 1);
+
+  if (tid == 0) {
+    for (int i = 0; i < G8LS_NST; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sempty[i], 1);
+    }
+    mbar_init(afull, 1);
+    mbar_init(aempty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512u)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  constexpr uint32_t tmem = 0;
+  if (tid == 0 && *tmem_slot != 0u) __trap();
+
+  if (warp == 0) {
+    // ---- producer: the block's 12 planes, interleaved P_1 Q_1 P_2 Q_2 ...
+    if (lane == 0) {
+      for (int64_t k = 0; k < nblk; ++k) {
+        const int slot = (int)(k % G8LS_NST);
+        if (k >= G8LS_NST) mbar_wait(&sempty[slot], (uint32_t)(((k / G8LS_NST) - 1) & 1));
+        unsigned char* st = sm + slot * G8LS_STAGE;
+        const unsigned char* src = planes + (size_t)(b0 + k) * G8_BLOCK_BYTES;
+        mbar_arrive_expect_tx(&sfull[slot], (uint32_t)G8LS_STAGE);
+#pragma unroll
+        for (int d = 0; d < G8_ND; ++d) {
+          bulk_g2s(st + 2 * d * G8_PLANE, src + d * G8_PLANE, (uint32_t)G8_PLANE, &sfull[slot]);
+          bulk_g2s(st + (2 * d + 1) * G8_PLANE, src + (G8_ND + d) * G8_PLANE, (uint32_t)G8_PLANE, &sfull[slot]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- MMA issuer: one N = 256 MMA per digit pair of the CTA's level set
+    const uint32_t sbase = smem_u32(sm);
+    const uint32_t idesc = idesc_g8_n256();
+    for (int64_t k = 0; k < nblk; ++k) {
+      const int slot = (int)(k % G8LS_NST);
+      const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
+      if (first_in_period && k > 0) mbar_wait(aempty, (uint32_t)(((k / G8_FLUSH_BLOCKS) - 1) & 1));
+      mbar_wait(&sfull[slot], (uint32_t)((k / G8LS_NST) & 1));
+      tc_fence_after();
+      const uint32_t st = sbase + (uint32_t)(slot * G8LS_STAGE);
+      bool fresh0 = first_in_period, fresh1 = first_in_period;
+#pragma unroll
+      for (int p = 1; p <= G8_ND; ++p) {
+        const int q0 = lv0 - p, q1 = lv1 - p;
+        if (q0 >= 1 && q0 <= G8_ND) {
+          umma_i8_ss(tmem, umma_desc_sw32(st + (uint32_t)(2 * (p - 1) * G8_PLANE)),
+                     umma_desc_sw32(st + (uint32_t)(2 * (q0 - 1) * G8_PLANE)), idesc, fresh0 ? 0u : 1u);
+          fresh0 = false;
+        }
+        if (lv1 && q1 >= 1 && q1 <= G8_ND) {
+          umma_i8_ss(tmem + 256u, umma_desc_sw32(st + (uint32_t)(2 * (p - 1) * G8_PLANE)),
+                     umma_desc_sw32(st + (uint32_t)(2 * (q1 - 1) * G8_PLANE)), idesc, fresh1 ? 0u : 1u);
+          fresh1 = false;
+        }
+      }
+      umma_commit_elect(&sempty[slot]);
+      if ((k % G8_FLUSH_BLOCKS) == G8_FLUSH_BLOCKS - 1 || k == nblk - 1) umma_commit_elect(afull);
+      __syncwarp();
+    }
+  } else {
+    // ---- flush: thread = member i = TMEM lane; columns in chunks of 8
+    const int quad = warp & 3;
+    const int i = 32 * quad + lane;
+    const int64_t nper = (nblk + G8_FLUSH_BLOCKS - 1) / G8_FLUSH_BLOCKS;
+    double* prow = partial + (size_t)blockIdx.x * (2 * G8_N) * G8_N + i;  // column j at prow[j * G8_N]
+    // level l weighs 256^(8 - l) in units of level 8 (g8_combine's convention)
+    const double w0 = pow2(8 * (8 - lv0)), w1 = lv1 ? pow2(8 * (8 - lv1)) : 0.0;
+    for (int j = 0; j < 2 * G8_N; ++j) prow[(size_t)j * G8_N] = 0.0;
+    for (int64_t pd = 0; pd < nper; ++pd) {
+      mbar_wait(afull, (uint32_t)(pd & 1));
+      tc_fence_after();
+      for (int cg = 0; cg < 2 * G8_N / 8; ++cg) {
+        uint32_t v0[8], v1[8];
+        tmem_ld8(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(8 * cg), v0);
+        tmem_ld8(tmem + ((uint32_t)(32 * quad) << 16) + 256u + (uint32_t)(8 * cg), v1);
+        tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          prow[(size_t)(8 * cg + c) * G8_N] += fma((double)(int)v1[c], w1, (double)(int)v0[c] * w0);
+      }
+      tc_fence_before();
+      mbar_arrive(aempty);
+    }
+    // scales: 2^(e_i + f_j - 62) = 2^32 / (sc_i sc_j)  (see gram_i8_mma_kernel)
+    const double ai = 4294967296.0 / g8_scale(cmax[i]);
+    for (int j = 0; j < 2 * G8_N; ++j) prow[(size_t)j * G8_N] *= ai / g8_scale(cmax[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u) : "memory");
+  }
+}
+
+// Gram from the level-split partials [group][set][256][128]: fixed-order sum over
+// groups and the 4 level sets; V'V from its upper triangle (exactly symmetric).
+__global__ void gram_i8_ls_reduce(const double* __restrict__ partial, int ngroups, double s_vv, double s_vd,
+                                  const int* __restrict__ overflow, double* __restrict__ gram) {
+  if (*overflow) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= G8_N * 2 * G8_N) return;
+  const int i = e / (2 * G8_N), c = e % (2 * G8_N);
+  int a = i, b = c;
+  if (c < G8_N && i > c) { a = c; b = i; }
+  const double* src = partial + (size_t)b * G8_N + a;
+  double s = 0.0;
+  for (int g = 0; g < ngroups; ++g)
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) s += src[((size_t)g * 4 + rr) * G8_N * 2 * G8_N];
+  gram[e] = s * (c < G8_N ? s_vv : s_vd);
+}
+
 // Gram from the per-CTA partials [group][quarter][128][64]: fixed-order sum over
 // groups; the V'V block from its upper triangle (exactly symmetric); scales
 // s_vv = 1/(N-1), s_vd = 1/sqrt(N-1).  Skipped when the FP64 fallback ran.
