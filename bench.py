@@ -228,7 +228,7 @@ def run_ours(args):
     # reference's ISM sweep) and the MMA pass, over 3 extra steps after the timed region
     sweep_ms = None
     n_ens_ = n
-    if n_ens_ == 128 and os.environ.get("ENKF_GRAM", "i8") == "i8":
+    if n_ens_ == 128 and os.environ.get("ENKF_GRAM", "i8ls") in ("i8", "i8ls"):
         import ctypes
         from paper_1302_3876_b200 import _native
         lib = _native.lib()
@@ -375,8 +375,11 @@ def run_ours(args):
             "algorithmic": "per observed row: read X[idx] row and Y row (2*N*8 B), r and idx (16 B), write its "
                            "6+6 byte-digit planes (2*N*6 B) = 3600 B",
             "mma_pass_ms": sweep_ms[1]},
-        "gram_kernel": {"impl": ("gram_i8_slice_kernel + gram_i8_mma_kernel (exact byte-digit products on tcgen05 "
-                                 "kind::i8; ENKF_GRAM=fp64 selects the FP64 DMMA gram128_kernel)") if gram_i8 else
+        "gram_kernel": {"impl": ("gram_i8_slice_kernel + " +
+                                 ("gram_i8_mma_kernel (column split)" if os.environ.get("ENKF_GRAM") == "i8"
+                                  else "gram_i8_mma_ls_kernel (level split, N = 256 MMAs)") +
+                                 " (exact byte-digit products on tcgen05 kind::i8; ENKF_GRAM=fp64 selects the "
+                                 "FP64 DMMA gram128_kernel)") if gram_i8 else
                                 "gram128_kernel (FP64 DMMA)",
                         "fp64_equiv_tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None,
                         "fp64_equiv_frac_of_dmma_peak": (flop_gram / (t_gram * 1e-3) / 1e12) / FP64_DMMA_PEAK_TFLOPS

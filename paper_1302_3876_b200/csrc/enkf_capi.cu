@@ -43,8 +43,9 @@ struct enkf_plan {
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
-  bool gram_ls = false;                   // level-split N = 256 MMA pass (opt-in: ENKF_GRAM=i8ls)
+  bool gram_ls = true;                    // level-split N = 256 MMA pass (default; ENKF_GRAM=i8: column split)
   double* g8_ls_partial = nullptr;        // [groups][4][256][128] (level-split form)
+  int* g8_ls_progress = nullptr;          // [groups][4] blocks issued per CTA (level-split pacing)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
   bool tiny = true;                       // desk-scale problems: the whole step in one CTA (ENKF_TINY=0: off)
   char* small_h = nullptr;                // host path for small problems: page-locked staging block
@@ -282,8 +283,11 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
       return e;
+    if (!p->g8_ls_progress && (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemsetAsync(p->g8_ls_progress, 0, sizeof(int) * 4 * p->g8_groups, s)) != cudaSuccess) return e;
     gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
-                                                                       p->g8_ls_partial, overflow);
+                                                                       p->g8_ls_partial, overflow, p->g8_ls_progress);
   } else {
     const size_t smem = gram_i8_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
@@ -652,7 +656,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
     p->gram_fused = (strcmp(env, "i8fused") == 0);
-    p->gram_ls = (strcmp(env, "i8ls") == 0);
+    p->gram_ls = (strcmp(env, "i8") != 0);  // ENKF_GRAM=i8: the column-split MMA pass
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
@@ -739,6 +743,7 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->g8_meta);
   cudaFree(p->g8_partial);
   cudaFree(p->g8_ls_partial);
+  cudaFree(p->g8_ls_progress);
   cudaFree(p->cyc_status);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);

@@ -654,6 +654,7 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
 constexpr int G8LS_NST = 4;                        // 48 KiB stages
 constexpr int G8LS_STAGE = 2 * G8_ND * G8_PLANE;   // P_1 Q_1 ... P_6 Q_6
 constexpr int G8LS_THREADS = 6 * 32;
+constexpr int G8LS_LEAD = 48;                      // max blocks a CTA runs ahead of its group
 __host__ __device__ constexpr size_t gram_i8_ls_smem_bytes() {
   return (size_t)G8LS_NST * G8LS_STAGE + (2 * G8LS_NST + 2) * 8 + 16 + 1024;
 }
@@ -669,7 +670,7 @@ __device__ __forceinline__ int g8ls_level(int r, int k) {
 __global__ void __launch_bounds__(G8LS_THREADS, 1)
 gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned long long* __restrict__ cmax,
                       int64_t n_blocks, int64_t blocks_per_group, double* __restrict__ partial,
-                      const int* __restrict__ overflow) {
+                      const int* __restrict__ overflow, int* __restrict__ progress /* [groups][4], zeroed */) {
   if (*overflow) return;  // the FP64 fallback computes the Gram
   extern __shared__ __align__(1024) unsigned char g8sm_raw[];
   unsigned char* sm = g8sm_raw + ((1024u - (smem_u32(g8sm_raw) & 1023u)) & 1023u);
@@ -711,9 +712,22 @@ gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned l
 
   if (warp == 0) {
     // ---- producer: the block's 12 planes, interleaved P_1 Q_1 P_2 Q_2 ...
+    //      The 4 CTAs of a group carry 6, 6, 7, 7 pairs per block; the producer of a
+    //      CTA that runs ahead waits (bounded: a hint, never a correctness barrier)
+    //      until the group's slowest CTA is within G8LS_LEAD blocks, so each image is
+    //      read from DRAM once and served from L2 to the other three.
     if (lane == 0) {
+      const volatile int* gp = progress + grp * 4;
+      int known = 0;  // last group minimum read: poll (~1-2 us of L2 latency) only when needed
       for (int64_t k = 0; k < nblk; ++k) {
         const int slot = (int)(k % G8LS_NST);
+        if ((int)k - G8LS_LEAD > known) {
+          for (int spin = 0; spin < (1 << 16); ++spin) {
+            known = min(min(gp[0], gp[1]), min(gp[2], gp[3]));
+            if (known >= (int)k - G8LS_LEAD) break;
+            __nanosleep(256);
+          }
+        }
         if (k >= G8LS_NST) mbar_wait(&sempty[slot], (uint32_t)(((k / G8LS_NST) - 1) & 1));
         unsigned char* st = sm + slot * G8LS_STAGE;
         const unsigned char* src = planes + (size_t)(b0 + k) * G8_BLOCK_BYTES;
@@ -753,8 +767,10 @@ gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned l
       }
       umma_commit_elect(&sempty[slot]);
       if ((k % G8_FLUSH_BLOCKS) == G8_FLUSH_BLOCKS - 1 || k == nblk - 1) umma_commit_elect(afull);
+      if (lane == 0) *(volatile int*)(progress + grp * 4 + r) = (int)(k + 1);
       __syncwarp();
     }
+    if (lane == 0) *(volatile int*)(progress + grp * 4 + r) = 0x7fffffff;  // done: never the minimum
   } else {
     // ---- flush: thread = member i = TMEM lane; columns in chunks of 8
     const int quad = warp & 3;
