@@ -639,7 +639,8 @@ gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long
 }
 
 // ---------------------------------------------------------------------------
-// Level-split MMA pass (opt-in, ENKF_GRAM=i8ls).  The 4 CTAs of a group split the
+// Level-split MMA pass (default; ENKF_GRAM=i8 selects the column-split
+// gram_i8_mma_kernel above).  The 4 CTAs of a group split the
 // digit pairs by level l = p + q instead of by output column: CTA r owns the level
 // set G8LS_SETS[r] ({7}, {8, 2}, {6, 3}, {5, 4}: 6, 6, 7, 7 pairs) for all 256
 // output columns [P'P | P'Q], in two 256-column int32 accumulators (all of TMEM).
