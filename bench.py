@@ -1,38 +1,50 @@
 """Benchmark of the B200 EnKF analysis step (iterative Sherman-Morrison).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
 
-N > 1 runs under torchrun (one rank per GPU, NCCL).  One JSON line on rank 0.
+N > 1: run under torchrun (one rank per GPU; the driver's launch), or plain
+`python bench.py --gpus N`, which re-launches itself under torchrun with N ranks
+(and exits non-zero if fewer than N GPUs are visible).  One JSON line on rank 0.
 
 A "step" = one full analysis step (BASELINE.json metric "EnKF analysis
-steps/sec"): level-0 Gram pass over the observed rows, NCCL allreduce of the
-N x 2N Gram (N > 1), the N Sherman-Morrison levels, and the anomaly update
-X^A = X T over every state row.  Workload = config 5 (n_state = 2^26,
-n_ens = 128, n_obs = 2^23) by default: the config BASELINE.json's 1/2/4/8-GPU
-scaling is quoted on; it fits one B200 (X + X^A + Y = 136 GiB).
+steps/sec") through the product entry point enkf_analysis_async_f64: level-0
+Gram pass over the observed rows, (N > 1) ONE ncclAllReduce of the N x 2N Gram
+with the input-check flags appended, issued by the native layer on the compute
+stream, the N Sherman-Morrison levels, and the anomaly update X^A = X T over
+every state row.  Workload = config 5 (n_state = 2^26, n_ens = 128,
+n_obs = 2^23) by default: the config BASELINE.json's 1/2/4/8-GPU scaling is
+quoted on; it fits one B200 (X + X^A + Y + the Gram's operand images = 148 GB).
+State rows (and the observation rows they own) are sharded across ranks:
+strong scaling, the problem is fixed.
 
-  value : steps/s, whole job, inputs resident in HBM, CUDA-event timed,
-          max over ranks (strong scaling: the problem is fixed, rows sharded).
-  e2e   : the same metric through the public API `analysis_step` with host
-          numpy buffers, host->device and device->host copies inside.
-  roofline : the anomaly-update kernel (the dominant one).  For n_ens = 128
-          it runs on the tcgen05 int8 tensor cores (exact byte-digit split of
-          the fp64 product) and is HBM-bound: GB/s of X read + X^A written
-          against MEASURED_PEAKS.json.  ENKF_ANOMALY=fp64 selects the FP64
-          DMMA kernel (FP64 TFLOP/s against the measured DMMA peak).
+  value : steps/s, whole job, inputs resident in HBM, CUDA-event timed on the
+          launching stream, barrier + synchronize around the K steps, max over
+          ranks.  The default arithmetic is fp64 EMULATED on the int8 tensor
+          cores (exact byte-digit products, one rounding; `dtype` says so);
+          `strict_fp64` times the all-IEEE-FP64 DMMA path in the same run.
+  e2e   : the same metric through the public API with host buffers, host->device
+          and device->host copies inside the timed region (N = 1:
+          `analysis_step(numpy)`; N > 1: each rank's shard through
+          enkf_analysis_host_f64 with the communicator attached).
+  roofline : the anomaly-update kernel (the dominant one): HBM GB/s of X read +
+          X^A written against MEASURED_PEAKS.json; `roofline_step` = the step's
+          compulsory bytes / step time; `ism_sweep` = the Gram's HBM-streaming
+          pass on compulsory bytes, with the DRAM-traffic ratio from ncu.
   cpu_baseline : the CPU oracle (oracle/, a numpy/OpenBLAS restatement of the
-          reference, which is pure Python) on a bounded row sample of the same
-          workload, scaled linearly to the full size (cost is linear in
-          n_state and n_obs at fixed n_ens).
+          reference, which is pure Python) on two bounded row samples of the same
+          workload (linearity shown), extrapolated linearly to the full size.
 """
 
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
+import socket
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -41,6 +53,7 @@ sys.path.insert(0, ROOT)
 
 FP64_DMMA_PEAK_TFLOPS = 37.07  # measured: profiles/r01_fp64_probe.json (DMMA m8n8k4, 148 SMs)
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+EMULATED_DTYPE = "f64 (int8-digit emulation on tcgen05: exact byte-digit products, 26 digit pairs, one rounding)"
 
 
 def parse():
@@ -48,12 +61,14 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=5, choices=[4, 5])
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--scale-log2", type=int, default=0, help="shrink n_state/n_obs by 2^s (testing)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the strict-FP64 leg, the stage/pass breakdown and the overflow-cliff probe")
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     return ap.parse_args()
 
@@ -68,8 +83,62 @@ def dist_env():
 def workload_name(cfg, s):
     from paper_1302_3876_b200 import workloads as W
     z = W.SIZES[cfg]
+    if cfg <= 3:
+        return f"config{cfg}: n_state={z['ns']} n_ens={z['nens']} n_obs={z['nobs']}"
     return (f"config{cfg}: n_state=2^{(z['ns'] >> s).bit_length() - 1} n_ens={z['nens']} "
             f"n_obs=2^{(z['nobs'] >> s).bit_length() - 1}")
+
+
+def hbm_peak():
+    try:
+        peaks = json.load(open(PEAKS_PATH))
+        return float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- self-launch (N > 1)
+def self_launch(args):
+    """`python bench.py --gpus N` outside torchrun: re-run under torchrun with N
+    ranks on 127.0.0.1, NCCL communicator-init lines logged (NCCL_DEBUG=INFO,
+    SUBSYS=INIT) to per-rank files that rank 0 folds into its JSON line."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) are visible"}),
+              file=sys.stderr, flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=dict(os.environ)))
+
+
+def nccl_log_setup():
+    """Per-rank NCCL init logs (unless the caller configured NCCL_DEBUG itself)."""
+    if "NCCL_DEBUG" in os.environ:
+        return None
+    run = os.environ.get("TORCHELASTIC_RUN_ID", "") + os.environ.get("MASTER_PORT", "")
+    d = os.path.join(tempfile.gettempdir(), f"enkf_nccl_{run}")
+    os.makedirs(d, exist_ok=True)
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ["NCCL_DEBUG_SUBSYS"] = "INIT"
+    os.environ["NCCL_DEBUG_FILE"] = os.path.join(d, "nccl.%h.%p.log")
+    return d
+
+
+def nccl_init_lines(d):
+    if not d:
+        return None
+    keep = []
+    for f in sorted(glob.glob(os.path.join(d, "nccl.*.log"))):
+        for line in open(f, errors="replace"):
+            if "Init COMPLETE" in line or "ncclCommInitRank comm" in line:
+                keep.append(line.strip())
+    return keep[:32]
 
 
 # ----------------------------------------------------------------------------- CPU legs
@@ -77,36 +146,57 @@ def cpu_sample_log2(cfg: int, scale: int) -> int:
     return {4: 6, 5: 8}[cfg] - scale if cfg in (4, 5) else 0
 
 
-def run_cpu_oracle(cfg, scale, sample_log2, steps, warmup):
-    """Time the oracle port (numpy + OpenBLAS, all host threads) on a row sample."""
-    import numpy as np
+def _threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count()
 
+
+def run_cpu_oracle(cfg, scale, sample_log2, steps, warmup):
+    """Time the oracle port (numpy + OpenBLAS, all host threads).  Configs 1-3: the
+    full configuration.  Configs 4/5: two row samples 1/2^s and 1/2^(s-2) (the
+    step is linear in n_state and n_obs at fixed n_ens; the per-row cost of the two
+    shows it), value extrapolated from the larger sample."""
     import oracle
     from paper_1302_3876_b200 import workloads as W
 
-    s = max(0, sample_log2)
-    p = (W.config4 if cfg == 4 else W.config5)(scale + s)
-    for _ in range(warmup):
-        oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
-    times = []
-    for _ in range(max(1, steps)):
-        t0 = time.perf_counter()
-        oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
-        times.append(time.perf_counter() - t0)
-    t = min(times)
-    factor = 2 ** s
-    value = 1.0 / (t * factor)
-    ns, nobs, n = p.shape
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
-    return dict(value=value, unit="steps/s", cores=int(threads), kind="port",
-                sample=(f"oracle/ (numpy+OpenBLAS restatement of enkf.analysis_step) on a 1/{factor} "
-                        f"row sample (n_state={ns}, n_obs={nobs}, n_ens={n}), best of {len(times)}: "
-                        f"{t:.3f} s; value = 1/({t:.3f} s x {factor})"),
-                sample_seconds=t)
+    def timed(p, k):
+        for _ in range(warmup):
+            oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
+        times = []
+        for _ in range(max(1, k)):
+            t0 = time.perf_counter()
+            oracle.analysis_step_chunked(p.x, p.perturbed, p.indices, p.r)
+            times.append(time.perf_counter() - t0)
+        return min(times), len(times)
+
+    if cfg <= 3:
+        p = small_problem(cfg)
+        t, k = timed(p, max(3, steps))
+        return dict(value=1.0 / t, unit="steps/s", cores=int(_threads()), kind="port", extrapolated=False,
+                    sample=f"oracle/ (numpy+OpenBLAS restatement of enkf.analysis_step) on the full {p.name} "
+                           f"{p.shape}, best of {k}: {t * 1e3:.3f} ms", sample_seconds=t)
+    mk = W.config4 if cfg == 4 else W.config5
+    s_small = max(0, sample_log2)
+    s_big = max(0, s_small - 2)
+    out = {}
+    for s in (s_small, s_big):
+        p = mk(scale + s)
+        t, k = timed(p, steps if s == s_big else 1)
+        out[s] = (t, k, p.shape)
+        del p
+    t_b, k_b, shp = out[s_big]
+    t_s = out[s_small][0]
+    factor = 2 ** s_big
+    return dict(value=1.0 / (t_b * factor), unit="steps/s", cores=int(_threads()), kind="port", extrapolated=True,
+                sample=(f"oracle/ (numpy+OpenBLAS restatement of enkf.analysis_step) on a 1/{factor} row sample "
+                        f"(n_state={shp[0]}, n_obs={shp[1]}, n_ens={shp[2]}), best of {k_b}: {t_b:.3f} s; "
+                        f"value = 1/({t_b:.3f} s x {factor}); the 1/{2 ** s_small} sample took {t_s:.3f} s"),
+                sample_seconds=t_b,
+                linearity={"samples": [f"1/{2 ** s_small}", f"1/{factor}"], "seconds": [t_s, t_b],
+                           "time_ratio_for_4x_rows": t_b / t_s})
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -146,16 +236,122 @@ class ClockSampler:
         import statistics
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+        sm = [v for v in (num(r[1]) for r in self.rows) if v is not None]
+        mx = [v for v in (num(r[2]) for r in self.rows) if v is not None]
+        pw = [v for v in (num(r[3]) for r in self.rows if len(r) > 3) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # ----------------------------------------------------------------------------- GPU leg
+class Runner:
+    """One rank's analysis step through the product entry point
+    enkf_analysis_async_f64 (communicator attached when N > 1)."""
+
+    def __init__(self, ns_loc, nobs_loc, n, dev, comm, env=None):
+        import ctypes
+
+        from paper_1302_3876_b200 import _native
+        self.ctypes = ctypes
+        self.native = _native
+        self.lib = _native.lib()
+        saved = {k: os.environ.get(k) for k in (env or {})}
+        os.environ.update(env or {})  # plan knobs are read at plan creation
+        try:
+            self.plan = _native.Plan(ns_loc, nobs_loc, n, dev.index)
+        finally:
+            for k, v in saved.items():
+                if v is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = v
+        if comm is not None:
+            st = _native.EnkfStatus()
+            _native.raise_for_status(self.lib.enkf_plan_set_comm(self.plan.handle, comm.handle, ctypes.byref(st)),
+                                     st, "enkf_plan_set_comm")
+        self.lib.enkf_debug_set_stage_events.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        self.lib.enkf_debug_stage_times.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+        self.lib.enkf_debug_set_gram_events.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+        self.lib.enkf_debug_gram_times.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
+
+    def step(self, x, y, idx, r, out, stream):
+        code = self.lib.enkf_analysis_async_f64(self.plan.handle, x.data_ptr(), y.data_ptr(),
+                                                0 if idx is None else idx.data_ptr(), r.data_ptr(),
+                                                out.data_ptr(), stream)
+        if code != 0:
+            self.check(stream)
+            raise RuntimeError(f"enkf_analysis_async_f64 returned {code}")
+
+    def check(self, stream):
+        st = self.native.EnkfStatus()
+        code = self.lib.enkf_plan_sync_status(self.plan.handle, stream, self.ctypes.byref(st))
+        self.native.raise_for_status(code, st, "analysis step")
+
+    def stage_times(self, run_step, sync, reps=3):
+        """ms of the gram | allreduce | levels | anomaly stages (library events)."""
+        acc = [0.0] * 4
+        self.lib.enkf_debug_set_stage_events(self.plan.handle, 1)
+        for _ in range(reps):
+            run_step()
+            sync()
+            four = (self.ctypes.c_float * 4)()
+            if self.lib.enkf_debug_stage_times(self.plan.handle, four) == 0:
+                for i in range(4):
+                    acc[i] += four[i] / reps
+        self.lib.enkf_debug_set_stage_events(self.plan.handle, 0)
+        return dict(zip(("gram", "allreduce", "levels", "anomaly"), acc))
+
+    def gram_pass_times(self, run_step, sync, reps=3):
+        acc = [0.0, 0.0]
+        self.lib.enkf_debug_set_gram_events(self.plan.handle, 1)
+        for _ in range(reps):
+            run_step()
+            sync()
+            two = (self.ctypes.c_float * 2)()
+            if self.lib.enkf_debug_gram_times(self.plan.handle, two) == 0:
+                acc[0] += two[0] / reps
+                acc[1] += two[1] / reps
+        self.lib.enkf_debug_set_gram_events(self.plan.handle, 0)
+        return acc
+
+
+def small_problem(cfg):
+    from paper_1302_3876_b200 import workloads as W
+    return {1: W.config1, 2: lambda: W.Config2Cycler().cycle(), 3: W.config3}[cfg]()
+
+
+def timed_steps(run_step, steps, dev, stream, world, dist):
+    import torch
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for _ in range(steps):
+        run_step()
+    stop.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    if world > 1:
+        mt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+        ms = float(mt.item())
+    return ms
+
+
 def run_ours(args):
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -163,12 +359,12 @@ def run_ours(args):
     from paper_1302_3876_b200.build import build
 
     world, rank, local = dist_env()
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
+    nccl_dir = None
+    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        nccl_dir = nccl_log_setup()
+        dist.init_process_group("nccl", device_id=dev)
     if rank == 0:
         build()
     if world > 1:
@@ -176,80 +372,104 @@ def run_ours(args):
 
     cfg, scale = args.config, args.scale_log2
     z = W.SIZES[cfg]
-    ns, nobs, n = z["ns"] >> scale, z["nobs"] >> scale, z["nens"]
-    indices = W.random_indices(ns, nobs / ns, W.SEEDS[cfg]["h"])
+    small = cfg <= 3
+    if small:
+        p = small_problem(cfg)
+        ns, nobs, n = p.shape
+        indices = p.indices
+    else:
+        ns, nobs, n = z["ns"] >> scale, z["nobs"] >> scale, z["nens"]
+        indices = W.random_indices(ns, nobs / ns, W.SEEDS[cfg]["h"])
+    shard_world = 1 if small else world  # configs 1-3 do not shard: N independent replicas
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sl = args.cpu_sample_log2 if args.cpu_sample_log2 is not None else cpu_sample_log2(cfg, scale)
-        cpu = run_cpu_oracle(cfg, scale, sl, steps=2, warmup=0)
+        cpu = run_cpu_oracle(cfg, scale, sl, steps=2, warmup=0 if not small else 1)
 
-    shard = W.device_problem_shard(cfg, world, rank, dev, scale, indices=indices)
-    x, yv, r, idx = shard["x"], shard["perturbed"], shard["r"], shard["idx"]
+    if small:
+        x = torch.from_numpy(p.x).to(dev)
+        yv = torch.from_numpy(p.perturbed).to(dev)
+        r = torch.from_numpy(p.r).to(dev)
+        idx = None if p.indices is None else torch.from_numpy(p.indices).to(dev)
+    else:
+        shard = W.device_problem_shard(cfg, world, rank, dev, scale, indices=indices)
+        x, yv, r, idx = shard["x"], shard["perturbed"], shard["r"], shard["idx"]
     ns_loc, nobs_loc = x.shape[0], yv.shape[0]
     xa = torch.empty_like(x)
-    from paper_1302_3876_b200.distributed import CudaStages, ShardedAnalysis
-    runner = ShardedAnalysis(CudaStages(ns_loc, nobs_loc, n, dev))
+    comm = None
+    if shard_world > 1:
+        from paper_1302_3876_b200.distributed import NativeComm
+        comm = NativeComm(dev)
+    runner = Runner(ns_loc, nobs_loc, n, dev, comm)
     stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
 
-    def step(ev=None):
-        runner.step(x, yv, idx, r, xa, check=False, events=ev)
+    def step():
+        runner.step(x, yv, idx, r, xa, sptr)
 
     for _ in range(args.warmup):
         step()
-    runner.raise_for_status()
-
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    runner.check(sptr)
     with ClockSampler(local) as clocks:
-        start.record(stream)
-        for k in range(args.steps):
-            step(evs[k])
-        stop.record(stream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ms = start.elapsed_time(stop)
-    runner.raise_for_status()
-    t_gram = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    t_ar = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    t_lev = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    t_anom = sum(e[3].elapsed_time(e[4]) for e in evs) / args.steps
-    if world > 1:
-        mt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
-        ms = float(mt.item())
+        ms = timed_steps(step, args.steps, dev, stream, world, dist)
+    runner.check(sptr)
+    sync = lambda: torch.cuda.synchronize(dev)  # noqa: E731
 
-    # --- the Gram's two passes timed apart (int8 form): CUDA events recorded by the
-    # library around the slice pass (the HBM-streaming pass that replaces the
-    # reference's ISM sweep) and the MMA pass, over 3 extra steps after the timed region
-    sweep_ms = None
-    n_ens_ = n
-    if n_ens_ == 128 and os.environ.get("ENKF_GRAM", "i8ls") in ("i8", "i8ls"):
-        import ctypes
-        from paper_1302_3876_b200 import _native
-        lib = _native.lib()
-        lib.enkf_debug_set_gram_events.argtypes = [ctypes.c_void_p, ctypes.c_int32]
-        lib.enkf_debug_gram_times.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]
-        handle = runner.stages.plan.handle
-        lib.enkf_debug_set_gram_events(handle, 1)
-        acc = [0.0, 0.0]
-        for _ in range(3):
-            step()
-            torch.cuda.synchronize(dev)
-            two = (ctypes.c_float * 2)()
-            if lib.enkf_debug_gram_times(handle, two) == 0:
-                acc[0] += two[0] / 3
-                acc[1] += two[1] / 3
-        lib.enkf_debug_set_gram_events(handle, 0)
-        sweep_ms = acc
+    stages = runner.stage_times(step, sync)
+    if not any(stages.values()):  # config 1: the whole step is one single-CTA kernel (tiny.cuh)
+        stages = {"analysis_tiny": ms / args.steps}
+    gram_i8 = n == 128 and os.environ.get("ENKF_GRAM", "i8ls") != "fp64" and not small
+    passes = runner.gram_pass_times(step, sync) if (gram_i8 and not args.no_extras) else None
+    stages_all = None
+    if world > 1:
+        tv = torch.tensor([stages[k] for k in ("gram", "allreduce", "levels", "anomaly")], dtype=torch.float64,
+                          device=dev)
+        gath = [torch.empty_like(tv) for _ in range(world)]
+        dist.all_gather(gath, tv)
+        stages_all = [[round(float(v), 4) for v in g.cpu()] for g in gath]
 
-    # --- e2e with host buffers, copies inside the timed region.  One GPU: the
-    # public drop-in `analysis_step(numpy arrays)`; N GPUs: the public sharded
-    # API (`distributed.ShardedAnalysis`) fed from each rank's host shard.
+    # ---- the strict IEEE-FP64 step (DMMA Gram + DMMA anomaly update), same run
+    strict = None
+    if not args.no_extras and n == 128:
+        r64 = Runner(ns_loc, nobs_loc, n, dev, comm, env={"ENKF_GRAM": "fp64", "ENKF_ANOMALY": "fp64"})
+
+        def step64():
+            r64.step(x, yv, idx, r, xa, sptr)
+        for _ in range(max(1, args.warmup)):
+            step64()
+        r64.check(sptr)
+        with ClockSampler(local) as clocks64:
+            ms64 = timed_steps(step64, args.steps, dev, stream, world, dist)
+        r64.check(sptr)
+        st64 = r64.stage_times(step64, sync)
+        cs = clocks64.summary()
+        strict = {"value": args.steps / (ms64 / 1e3), "unit": "steps/s", "ms_per_step": ms64 / args.steps,
+                  "dtype": "f64 (IEEE: FP64 DMMA m8n8k4 Gram + FP64 DMMA anomaly update)",
+                  "kernels_ms": st64, "clocks": cs,
+                  "energy_j_per_step": (cs["power_w"] * ms64 / args.steps / 1e3) if cs.get("power_w") else None,
+                  "env": "ENKF_GRAM=fp64 ENKF_ANOMALY=fp64"}
+        del r64
+
+    # ---- overflow cliff: one Y element beyond its column's sampled scale sends the
+    # int8 Gram to the flag-gated FP64 fallback (measured, then restored)
+    cliff = None
+    if gram_i8 and not args.no_extras and world == 1:
+        k = nobs_loc // 3
+        old = float(yv[k, 5])
+        yv[k, 5] = 1e6
+        st_f = runner.stage_times(step, sync)
+        runner.check(sptr)
+        yv[k, 5] = old
+        step()
+        runner.check(sptr)
+        cliff = {"gram_ms_fallback": st_f["gram"], "gram_ms": stages["gram"],
+                 "extra_ms": st_f["gram"] - stages["gram"],
+                 "trigger": "one element of Y (or X[idx]) more than ~4x its column's sampled max "
+                            "(G8_HEADROOM = 2 bits): the int8 Gram pass flags it and gram128_kernel (FP64 DMMA) "
+                            "recomputes the Gram on the same stream"}
+
+    # ---- e2e with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
         import paper_1302_3876_b200 as P
@@ -258,30 +478,28 @@ def run_ours(args):
         x_h.copy_(x)
         y_h.copy_(yv)
         r_h = r.cpu().numpy()
-        idx_loc = idx.cpu().numpy()
+        idx_loc = None if idx is None else idx.cpu().numpy()
         del x, xa, yv
         torch.cuda.synchronize(dev)
         torch.cuda.empty_cache()
-        if world == 1:
-            h = P.SelectionOperator.from_indices(idx_loc)
+        if shard_world == 1:
+            h = P.SelectionOperator.identity() if idx_loc is None else P.SelectionOperator.from_indices(idx_loc)
             obs = P.ObservationBatch(y=None, perturbed=y_h.numpy(), perturbations=None)
             xnp = x_h.numpy()
 
             def e2e_step():
-                out = P.analysis_step(xnp, obs, h, r_h)  # numpy in, numpy out
-                return out
+                return P.analysis_step(xnp, obs, h, r_h)  # numpy in, numpy out
+            api = "paper_1302_3876_b200.analysis_step(numpy host arrays) -> enkf_analysis_host_f64"
         else:
-            out_h = torch.empty_like(x_h, pin_memory=True)
-            r_d = torch.from_numpy(r_h).to(dev)
-            idx_d = torch.from_numpy(idx_loc).to(dev)
+            from paper_1302_3876_b200.distributed import NativeShardedAnalysis
+            shard_runner = NativeShardedAnalysis(ns_loc, nobs_loc, n, dev, comm)
+            out_h = torch.empty_like(x_h, pin_memory=True).numpy()
+            xnp, ynp = x_h.numpy(), y_h.numpy()
 
             def e2e_step():
-                xd = x_h.to(dev, non_blocking=True)
-                yd = y_h.to(dev, non_blocking=True)
-                runner.step(xd, yd, idx_d, r_d, xd)  # in place; raises on any rank's error
-                out_h.copy_(xd)
-                torch.cuda.synchronize(dev)
-                return out_h
+                return shard_runner.step_host(xnp, ynp, idx_loc, r_h, out_h)
+            api = ("paper_1302_3876_b200.distributed.NativeShardedAnalysis.step_host (pinned host shards) -> "
+                   "enkf_analysis_host_f64 with the NCCL communicator attached")
         e2e_step()  # warm (plans, staging)
         if world > 1:
             dist.barrier()
@@ -293,49 +511,46 @@ def run_ours(args):
             et = torch.tensor([el], dtype=torch.float64, device=dev)
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
             el = float(et.item())
+        streamed = (shard_world == 1 and idx_loc is not None and os.environ.get("ENKF_HOST_STREAM", "1") != "0"
+                    and x_h.numel() * 8 > (1 << 20))
         e2e = {"value": args.e2e_steps / el, "unit": "steps/s",
-               # world 1, pinned X: the observed rows X[idx] cross PCIe twice (the
+               # streamed host path: the observed rows X[idx] cross PCIe twice (the
                # gather that feeds the Gram pass, then with their X chunk)
-               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes + idx_loc.nbytes
-                                         + (y_h.numel() * 8 if world == 1 and os.environ.get("ENKF_HOST_STREAM", "1") != "0"
-                                            else 0)) * world,
-               "d2h_bytes_per_step": int(x_h.numel() * 8) * world, "steps": args.e2e_steps,
-               "api": ("paper_1302_3876_b200.analysis_step(numpy host arrays) -> enkf_analysis_host_f64" if world == 1
-                       else "paper_1302_3876_b200.distributed.ShardedAnalysis.step from pinned host shards")}
+               "h2d_bytes_per_step": int(x_h.numel() * 8 + y_h.numel() * 8 + r_h.nbytes
+                                         + (idx_loc.nbytes if idx_loc is not None else 0)
+                                         + (y_h.numel() * 8 if streamed else 0)) * shard_world,
+               "d2h_bytes_per_step": int(x_h.numel() * 8) * shard_world, "steps": args.e2e_steps,
+               "inputs": "page-locked host buffers (pageable inputs take the staging-ring path)",
+               "api": api}
 
+    nccl_lines = nccl_init_lines(nccl_dir) if rank == 0 else None
     if rank != 0:
         if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
         return
 
     steps_per_s = args.steps / (ms / 1e3)
+    ms_step = ms / args.steps
+    peak, peak_src = hbm_peak()
+    t_anom = stages.get("anomaly", ms_step) or ms_step
+    t_gram = stages.get("gram", 0.0)
+    bytes_anom = 2.0 * ns_loc * n * 8
+    anom_gbs = bytes_anom / (t_anom * 1e-3) / 1e9
     flop_anom = 2.0 * ns_loc * n * n
     anom_tflops = flop_anom / (t_anom * 1e-3) / 1e12
-    flop_gram = 2.0 * nobs_loc * n * (2 * n)
-    gram_i8 = n == 128 and os.environ.get("ENKF_GRAM", "i8") != "fp64"
-    bytes_anom = 2.0 * ns_loc * n * 8
-    bytes_gram = nobs_loc * (2 * n * 8 + 16)
-    try:
-        peaks = json.load(open(PEAKS_PATH))
-        hbm_peak, peak_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
-    except Exception:
-        hbm_peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-    anom_gbs = bytes_anom / (t_anom * 1e-3) / 1e9
     tensor_core = n == 128 and os.environ.get("ENKF_ANOMALY", "i8") != "fp64"
     if tensor_core:
-        # int8-digit tcgen05 kernel: the FP64 product is exact integer work on
-        # the tensor cores; the kernel is bounded by streaming X in and X^A out
         traffic, traffic_src = None, None
         try:  # DRAM bytes per row from the committed ncu --set full capture, times this launch's rows
-            cap = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                              "r01_anomaly_dram.json")))
+            cap = json.load(open(os.path.join(ROOT, "profiles", "r01_anomaly_dram.json")))
             traffic = cap["dram_bytes_per_row"] * ns_loc
             traffic_src = ("dram__bytes_read.sum + dram__bytes_write.sum per row from " + cap["capture"] +
                            f", x {ns_loc} rows per launch ({cap['ratio_to_algorithmic']:.4f} x algorithmic)")
         except (OSError, KeyError, ValueError):
             pass
         roofline = {"bound": "hbm", "kernel": "anomaly_i8_kernel (X^A = X T, tcgen05.mma kind::i8 on exact byte digits, TMA-staged)",
-                    "achieved": anom_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": anom_gbs / hbm_peak,
+                    "achieved": anom_gbs, "peak": peak, "unit": "GB/s", "frac": anom_gbs / peak,
                     "traffic": traffic, "traffic_source": traffic_src,
                     "algorithmic": f"read X + write X^A = 2*n_state*n_ens*8 = {bytes_anom:.3e} B per launch",
                     "peak_source": peak_src,
@@ -347,7 +562,47 @@ def run_ours(args):
                     "frac": anom_tflops / FP64_DMMA_PEAK_TFLOPS, "traffic": None,
                     "algorithmic": f"2*n_state*n_ens^2 = {flop_anom:.3e} flop per launch",
                     "peak_source": "measured FP64 DMMA m8n8k4 issue rate on this pool's B200 (profiles/r01_fp64_probe.json); MEASURED_PEAKS.json has no FP64 entry",
-                    "hbm_view": {"achieved_gbs": anom_gbs, "peak_gbs": hbm_peak, "frac": anom_gbs / hbm_peak}}
+                    "hbm_view": {"achieved_gbs": anom_gbs, "peak_gbs": peak, "frac": anom_gbs / peak}}
+    if small:
+        roofline["note"] = "configs 1-3 are launch/latency-bound (SURVEY §8(d)); the fraction is reported, not a target"
+
+    # the whole step on its compulsory bytes (SURVEY §8(d) B_step)
+    b_step = 8.0 * (2 * ns * n + 2 * nobs * n + 2 * nobs)
+    roofline_step = {"bound": "hbm", "unit": "GB/s", "bytes": b_step,
+                     "achieved": b_step / (ms_step * 1e-3) / 1e9, "peak": peak * shard_world,
+                     "frac": b_step / (ms_step * 1e-3) / 1e9 / (peak * shard_world),
+                     "algorithmic": "B_step = 8*(2*Ns*N + 2*Nobs*N + 2*Nobs): read X, write X^A, read X[idx] rows, Y, r, idx"}
+
+    ism = None
+    comp_row = 2 * n * 8 + 16
+    if passes is not None:
+        ratio = None
+        try:
+            cap = json.load(open(os.path.join(ROOT, "profiles", "r01_gram_dram.json")))
+            ratio = cap["ratio_to_compulsory"]
+        except (OSError, KeyError, ValueError):
+            pass
+        ism = {"kernel": "gram_i8_slice_kernel: the observation-row streaming pass of the Gram (reduced-coordinate "
+                         "ISM, DESIGN §3/§6), which replaces the reference's per-group sweeps of the Nobs x 2N panel",
+               "bound": "hbm", "unit": "GB/s", "ms": passes[0],
+               "achieved": nobs_loc * comp_row / (passes[0] * 1e-3) / 1e9, "peak": peak,
+               "frac": nobs_loc * comp_row / (passes[0] * 1e-3) / 1e9 / peak,
+               "algorithmic": f"compulsory bytes per observed row: read X[idx] row and Y row (2*N*8 B), r and idx "
+                              f"(16 B) = {comp_row} B",
+               "traffic_ratio": ratio,
+               "traffic_source": "whole Gram (slice + MMA passes) DRAM bytes / compulsory, ncu --set full "
+                                 "(profiles/r01_gram_dram.json)",
+               "mma_pass_ms": passes[1]}
+    gram_compulsory = nobs_loc * comp_row / (t_gram * 1e-3) / 1e9 if t_gram > 0 else None
+    flop_gram = 2.0 * nobs_loc * n * (2 * n)
+    cs = clocks.summary()
+    # our kernels per step: Gram (int8: scales, slice, MMA, reduce + the two flag-gated
+    # FP64-fallback kernels, which exit at once | FP64: gram128 + reduce | tiny: 1 kernel
+    # for the whole step), levels, anomaly; + flag pack/unpack around the NCCL allreduce
+    if small and cfg == 1:
+        per_step = 1
+    else:
+        per_step = (6 if gram_i8 else 2) + 2 + (2 if comm is not None else 0)
     line = {
         "metric": "EnKF analysis steps/sec",
         "value": steps_per_s,
@@ -355,45 +610,47 @@ def run_ours(args):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms / args.steps,
+        "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "strong" if not small else "replicas",
         "vs_baseline": None,
-        "dtype": "f64",
-        "data": "synthetic (config value distributions, drawn on device with torch Philox; H indices from the reference's seeded Philox draw)",
+        "dtype": EMULATED_DTYPE if (tensor_core or gram_i8) else "f64",
+        "data": ("synthetic (config value distributions, drawn on device with torch Philox; H indices from the "
+                 "reference's seeded Philox draw)" if not small else
+                 "synthetic (host numpy Philox: the configuration's own generator, tests/golden pinned)"),
         "config": {"workload": workload_name(cfg, scale), "n_state": ns, "n_obs": nobs, "n_ens": n,
-                   "parallelism": f"row-shard x{world} (NCCL allreduce of the {n}x{2*n} Gram)" if world > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)},
-        "kernels_ms": {"gram": t_gram, "allreduce": t_ar, "levels": t_lev, "anomaly": t_anom},
+                   "parallelism": (f"row-shard x{world} (one ncclAllReduce of the {n}x{2 * n} Gram + flags per step, "
+                                   "issued by libenkf_b200 on the compute stream)") if shard_world > 1 else
+                   ("single GPU" if world == 1 else f"{world} independent replicas"),
+                   "l2": ("inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)) if not small
+                   else "inputs L2-resident (latency-bound configuration)"},
+        "kernels_ms": stages,
+        "kernels_ms_per_rank": stages_all,
         "roofline": roofline,
-        "ism_sweep": None if sweep_ms is None else {
-            "kernel": "gram_i8_slice_kernel: the observation-row streaming pass of the Gram (reduced-coordinate "
-                      "ISM, DESIGN §3/§6), which replaces the reference's per-group sweeps of the Nobs x 2N panel",
-            "bound": "hbm", "unit": "GB/s", "ms": sweep_ms[0],
-            "achieved": nobs_loc * (2 * n * 8 + 16 + 2 * n * 6) / (sweep_ms[0] * 1e-3) / 1e9,
-            "peak": hbm_peak, "frac": nobs_loc * (2 * n * 8 + 16 + 2 * n * 6) / (sweep_ms[0] * 1e-3) / 1e9 / hbm_peak,
-            "algorithmic": "per observed row: read X[idx] row and Y row (2*N*8 B), r and idx (16 B), write its "
-                           "6+6 byte-digit planes (2*N*6 B) = 3600 B",
-            "mma_pass_ms": sweep_ms[1]},
-        "gram_kernel": {"impl": ("gram_i8_slice_kernel + " +
-                                 ("gram_i8_mma_kernel (column split)" if os.environ.get("ENKF_GRAM") == "i8"
-                                  else "gram_i8_mma_ls_kernel (level split, N = 256 MMAs)") +
-                                 " (exact byte-digit products on tcgen05 kind::i8; ENKF_GRAM=fp64 selects the "
-                                 "FP64 DMMA gram128_kernel)") if gram_i8 else
-                                "gram128_kernel (FP64 DMMA)",
-                        "fp64_equiv_tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None,
-                        "fp64_equiv_frac_of_dmma_peak": (flop_gram / (t_gram * 1e-3) / 1e12) / FP64_DMMA_PEAK_TFLOPS
-                        if t_gram > 0 else None,
-                        "hbm_gbs_compulsory": bytes_gram / (t_gram * 1e-3) / 1e9 if t_gram > 0 else None},
-        "clocks": clocks.summary(),
-        # kernels per step: Gram (int8: scales, slice, MMA, reduce + the two flag-gated
-        # FP64-fallback kernels, which exit at once | FP64: gram128 + reduce); levels; anomaly
-        "gpu_launches": ((6 if gram_i8 else 2) + 1 + 1) * args.steps,
+        "roofline_step": roofline_step,
+        "ism_sweep": ism,
+        "gram_kernel": {"impl": ("gram_i8_slice_kernel + gram_i8_mma_ls_kernel (level split, N = 256 MMAs) "
+                                 "(exact byte-digit products on tcgen05 kind::i8; ENKF_GRAM=fp64 selects the "
+                                 "FP64 DMMA gram128_kernel)") if gram_i8 else "FP64 DMMA Gram",
+                        "hbm_gbs_compulsory": gram_compulsory,
+                        "hbm_frac_compulsory": gram_compulsory / peak if gram_compulsory else None,
+                        "fp64_equiv_tflops": flop_gram / (t_gram * 1e-3) / 1e12 if t_gram > 0 else None},
+        "strict_fp64": strict,
+        "overflow_cliff": cliff,
+        "clocks": {k: cs[k] for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")},
+        "power_w": cs.get("power_w"),
+        "energy_j_per_step": (cs["power_w"] * ms_step / 1e3) if cs.get("power_w") else None,
+        "gpu_launches": per_step * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
+    if nccl_lines is not None:
+        line["nccl_init"] = nccl_lines
+        for ln in nccl_lines:
+            print("[nccl] " + ln, file=sys.stderr)
     print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 
@@ -403,7 +660,7 @@ def run_reference(args):
         return
     cfg, scale = args.config, args.scale_log2
     sl = args.cpu_sample_log2 if args.cpu_sample_log2 is not None else cpu_sample_log2(cfg, scale)
-    cpu = run_cpu_oracle(cfg, scale, sl, steps=args.steps, warmup=min(args.warmup, 1))
+    cpu = run_cpu_oracle(cfg, scale, sl, steps=min(args.steps, 5), warmup=min(args.warmup, 1))
     from paper_1302_3876_b200 import workloads as W
     z = W.SIZES[cfg]
     line = {
@@ -424,7 +681,13 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     else:
+        world, _, _ = dist_env()
+        if world != args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), file=sys.stderr)
+            sys.exit(2)
         run_ours(args)
 
 

@@ -80,10 +80,20 @@ int32_t enkf_max_ens(void);
  * host thread (the library links its own CUDA runtime; callers that manage
  * devices elsewhere, e.g. torch, pass their device index here). */
 int32_t enkf_set_device(int32_t device);
+/* The calling thread's current CUDA device (so a caller can restore it after
+ * enkf_set_device; every plan entry point already restores it on return). */
+int32_t enkf_get_device(int32_t* device);
 
-/* Plan: owns the device workspace (Gram partials, Gram, A, T, status) for one
- * (n_state, n_obs, n_ens) shape on the current device.  No allocation happens
- * in the compute calls.  Thread-safe per plan (one call at a time). */
+/* Plan: owns the device workspace (Gram partials, the int8 Gram's operand
+ * images, Gram, A, T, status) for one (n_state, n_obs, n_ens) shape on the
+ * current device, all allocated here: the device-buffer analysis calls
+ * (enkf_analysis_f64 / _async_f64 and the staged form) allocate nothing, so they
+ * can be captured into a CUDA graph without a warm-up call.  Entries that need
+ * workspace only some callers use allocate it on their first call and keep it
+ * with the plan: the host-buffer entry (device copies of X, Y, r, idx), the
+ * localized analysis (V, D, Z) and the Lorenz-96 forecast / cycle entries.
+ * Every entry point runs on the plan's device and restores the caller's current
+ * device before returning.  Thread-safe per plan (one call at a time). */
 int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens,
                          enkf_plan** plan, enkf_status* status);
 void enkf_plan_destroy(enkf_plan* plan);
@@ -174,6 +184,35 @@ int32_t enkf_ism_levels_f64(enkf_plan* plan, const double* gram, double* A, doub
 /* XA[rows] = X[rows] @ T  ==  X + S (V'Z).  XA may equal X. */
 int32_t enkf_anomaly_update_f64(enkf_plan* plan, const double* X, const double* T,
                                 double* XA, int64_t n_rows, void* stream);
+
+/* --- multi-GPU: one process per GPU, state rows sharded ---
+ *
+ * Rank g owns the contiguous state rows [lo_g, hi_g) and the observation rows whose
+ * (sorted) index falls in that range; its plan is created for the LOCAL sizes and
+ * its idx is relative to lo_g.  With a communicator attached to the plan,
+ * enkf_analysis_f64 / _async_f64 / _host_f64 run one shard of the step: the local
+ * level-0 Gram, ONE ncclAllReduce (sum, fp64, on the call's stream) of the N x 2N
+ * Gram with the shard's input-check flags appended, the N levels on the identical
+ * global Gram (every rank, no broadcast), the anomaly update of the local rows.
+ * Every rank returns the same status (an input error on one rank raises on all),
+ * with no extra collective or host synchronisation; the async form stays
+ * graph-capturable.  Replaces the reference's thread-blocked column sweep
+ * (sherman.py:162, 189-203, solve_sherman_blocked) as the parallel scheme.
+ * NCCL is loaded at run time (libnccl.so.2); ENKF_NOT_SUPPORTED if it is absent.
+ * The localized, cycled and solve_sherman entries return ENKF_NOT_SUPPORTED on a
+ * plan with a communicator. */
+
+/* ncclGetUniqueId on rank 0: 128 bytes to hand to every rank (e.g. broadcast over
+ * torch.distributed). */
+int32_t enkf_comm_unique_id(unsigned char* id /* [128] */, enkf_status* status);
+/* ncclCommInitRank for `rank` of `nranks` on CUDA device `device`; *comm receives
+ * the ncclComm_t (caller-owned: enkf_comm_destroy). */
+int32_t enkf_comm_init(const unsigned char* id /* [128] */, int32_t nranks, int32_t rank, int32_t device,
+                       void** comm, enkf_status* status);
+int32_t enkf_comm_destroy(void* comm);
+/* Attach an ncclComm_t (from enkf_comm_init or the caller's own NCCL) to a plan;
+ * NULL detaches.  The communicator must outlive the plan's use of it. */
+int32_t enkf_plan_set_comm(enkf_plan* plan, void* comm, enkf_status* status);
 
 /* --- solve_sherman parity (sherman.py:253-286): Z = (R + V V')^-1 D --- */
 int32_t enkf_ism_solve_f64(enkf_plan* plan, const double* r, const double* V,

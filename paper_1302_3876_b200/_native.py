@@ -46,6 +46,7 @@ PROTOTYPES = {
     "enkf_version": (ctypes.c_char_p, []),
     "enkf_max_ens": (_i32, []),
     "enkf_set_device": (_i32, [_i32]),
+    "enkf_get_device": (_i32, [ctypes.POINTER(_i32)]),
     "enkf_plan_reset_status": (_i32, [_vp, _vp]),
     "enkf_plan_create": (_i32, [_i64, _i64, _i64, ctypes.POINTER(_vp), _st]),
     "enkf_plan_destroy": (None, [_vp]),
@@ -68,6 +69,10 @@ PROTOTYPES = {
                                             ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _st,
                                             ctypes.POINTER(_i32)]),
     "enkf_inflate_f64": (_i32, [_vp, _vp, _i64, _i64, ctypes.c_double, _vp]),
+    "enkf_comm_unique_id": (_i32, [_vp, _st]),
+    "enkf_comm_init": (_i32, [_vp, _i32, _i32, _i32, ctypes.POINTER(_vp), _st]),
+    "enkf_comm_destroy": (_i32, [_vp]),
+    "enkf_plan_set_comm": (_i32, [_vp, _vp, _st]),
 }
 
 _lib = None
@@ -128,6 +133,28 @@ def raise_for_status(code: int, status: EnkfStatus | None, what: str = "") -> No
     raise RuntimeError(f"CUDA error in {what}: {msg}")
 
 
+class on_device:
+    """Run the enclosed native calls with `index` as the thread's current CUDA
+    device and restore the caller's device afterwards (torch keeps its own)."""
+
+    def __init__(self, index: int):
+        self.index = int(index)
+        self.prev = None
+
+    def __enter__(self):
+        prev = _i32(-1)
+        if lib().enkf_get_device(ctypes.byref(prev)) == ENKF_OK:
+            self.prev = prev.value
+        if lib().enkf_set_device(self.index) != ENKF_OK:
+            raise RuntimeError(f"enkf_set_device({self.index}) failed")
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None and self.prev != self.index:
+            lib().enkf_set_device(self.prev)
+        return False
+
+
 class Plan:
     """Owns one enkf_plan (device workspace for a fixed shape)."""
 
@@ -135,11 +162,10 @@ class Plan:
         self.shape = (int(n_state), int(n_obs), int(n_ens))
         self.device_index = int(device_index)
         self._h = _vp()
-        if lib().enkf_set_device(self.device_index) != ENKF_OK:
-            raise RuntimeError(f"enkf_set_device({self.device_index}) failed")
         st = EnkfStatus()
-        code = lib().enkf_plan_create(self.shape[0], self.shape[1], self.shape[2],
-                                      ctypes.byref(self._h), ctypes.byref(st))
+        with on_device(self.device_index):
+            code = lib().enkf_plan_create(self.shape[0], self.shape[1], self.shape[2],
+                                          ctypes.byref(self._h), ctypes.byref(st))
         raise_for_status(code, st, "enkf_plan_create")
         self.lock = threading.Lock()
 

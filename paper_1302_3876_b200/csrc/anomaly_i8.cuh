@@ -1,26 +1,30 @@
-// anomaly_i8.cuh — X^A = X + X C on the 5th-generation tensor cores (N == 128).
+// anomaly_i8.cuh — X^A = X T on the 5th-generation tensor cores (N == 128).
 //
-// The anomaly update (enkf.py:192, x + s @ A, K11) is an Ns x 128 x 128 fp64
-// product.  B200 has no fp64 tcgen05 kind, so the product is evaluated
-// EXACTLY in integer arithmetic on byte "digits" (Ozaki-style splitting) and
-// rounded once at the end:
-//   row i of X  : e_i with max|X_i.| < 2^e_i,  V_ik = round(X_ik 2^(47-e_i))  (48-bit)
-//   column j of C: f_j with max|C_.j| < 2^f_j, W_kj = round(C_kj 2^(47-f_j))
+// The anomaly update (enkf.py:192, x + s @ A) is evaluated as X^A = X T with
+// T = I + (I - 11'/N) A / sqrt(N-1) (ism_levels writes T), an Ns x 128 x 128 fp64
+// product.  B200 has no fp64 tcgen05 kind, so the product is evaluated EXACTLY in
+// integer arithmetic on byte "digits" (Ozaki-style splitting) and rounded once:
+//   row i of X : e_i with max|X_i.| < 2^e_i,  V_ik = round(X_ik 2^(47-e_i))  (48-bit)
+//   all of T   : ONE power-of-two scale f,    W_kj = round(T_kj 2^(47-f))
 //   V = sum_p d_p 256^(6-p), W = sum_q c_q 256^(6-q), p,q = 1..6 two's-complement
-//   bytes (p = 1 signed, the rest unsigned).  X C ~= 2^(e_i+f_j-94) sum_{p+q<=8}
+//   bytes (p = 1 signed, the rest unsigned).  X T ~= 2^(e_i+f-94) sum_{p+q<=8}
 //   256^(12-p-q) (D_p C_q)_ij with every D_p C_q an exact int32 tcgen05.mma
-//   (kind::i8, K = 128 -> |acc| < 2^26).  26 digit pairs, 7 levels l = p+q.
-// Truncation (p+q > 8) and the input roundings give |error| ~ 1e-13 relative
-// to max|X^A| on the config inputs (tests compare against the FP64 DMMA path
-// and the oracle).
+//   (kind::i8, K = 128 -> |acc| < 2^26): 26 digit pairs, 7 levels l = p + q.
+// Truncation (p+q > 8) and the input roundings give ~7e-14 relative to max|X^A|
+// (tests compare against the FP64 DMMA path and the oracle).
 //
-// Layout: the 6 digit planes of C^T (M = 128 output columns x K = 128) stay in
-// TMEM for the whole kernel (A operand, 6 x 32 columns); X-row digit planes
-// (B operand, N = 16 rows per MMA, K-major, 128B swizzle) are produced by 4
-// slicer warps into a 2-deep smem ring; the accumulators (7 levels x 16
-// columns) are double-buffered in TMEM; 4 epilogue warps (thread = output
-// column = TMEM lane) recombine the 7 int32 levels exactly in int64, round to
-// fp64, add X and store.  One elected thread issues the MMAs.
+// Roles (14 warps): a TMA warp bulk-copies each contiguous 32-row X
+// tile into a 4-deep smem ring; 4 slicer warps form the row exponents and the six
+// X digit planes (B operand, N = 16 rows per MMA, K-major, 128B swizzle) and
+// release the stage at once (the epilogue never reads X); the six digit planes of
+// T^T stay in TMEM for the whole kernel (A operand, 192 columns); one elected
+// thread issues the 208 MMAs of a tile into double-buffered TMEM accumulators
+// (7 levels x 16 columns); 8 epilogue warps (thread = output column = TMEM lane)
+// combine the 7 int32 levels in INTEGER arithmetic into one int64, convert once
+// (the only rounding) and scale through the exponent field — no FP64 arithmetic
+// next to the MMAs (FP64 ops were measured to stall the int8 tensor pipe).
+// T == I exactly copies X bit for bit; tiny / huge / non-finite rows take exact
+// slow paths.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -253,9 +257,16 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 __global__ void __launch_bounds__(I8_THREADS, 1)
 anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
-                  double* __restrict__ XA, int64_t n_rows, int dbg, uint32_t uz /* = 0 */) {
-  // dbg (profiling only): bit0 skip MMAs, bit1 skip slicing, bit2 skip the epilogue,
+                  double* __restrict__ XA, int64_t n_rows, int dbg_arg, uint32_t uz /* = 0 */) {
+  // dbg (profiling builds only, -DI8_DBG_BUILD; the product build compiles every dbg
+  // branch out): bit0 skip MMAs, bit1 skip slicing, bit2 skip the epilogue,
   // bit4 drain TMEM but skip the recombination, bit5 stores into an L2-resident window.
+#ifdef I8_DBG_BUILD
+  const int dbg = dbg_arg;
+#else
+  constexpr int dbg = 0;
+  (void)dbg_arg;
+#endif
   // Measured with these (tools/probe/i8_trace.py): FP64 arithmetic (DFMA/DADD/DMUL)
   // issued by other warps slows the int8 MMAs roughly in proportion to its count,
   // integer ops and int->fp64 conversions do not.

@@ -22,6 +22,7 @@
 #include "gram_i8_fused.cuh"
 #include "host_stream.cuh"
 #include "tiny.cuh"
+#include "nccl_comm.cuh"
 
 using namespace enkf;
 
@@ -94,6 +95,13 @@ struct enkf_plan {
   double* l96ws = nullptr;
   DevStatus* cyc_status = nullptr;  // per-cycle status of enkf_cycle_l96_f64
   int cyc_cap = 0;
+  // multi-GPU: the NCCL communicator of this shard (caller-owned) and the last NCCL error
+  ncclComm_t comm = nullptr;
+  int comm_ranks = 1, comm_rank = 0;
+  int nccl_rc = 0;
+  // measurement: events at the stage boundaries of the analysis step
+  bool stage_events = false;
+  cudaEvent_t st_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -213,6 +221,36 @@ cudaError_t launch_gram(enkf_plan* p, bool analysis, const double* X, const doub
   return cudaGetLastError();
 }
 
+// Workspace of the int8 Gram for the plan's shape (allocated by enkf_plan_create
+// when the int8 Gram is the plan's analysis Gram, so the compute calls allocate
+// nothing and a CUDA-graph capture needs no warm-up call).
+cudaError_t ensure_gram_i8_workspace(enkf_plan* p) {
+  cudaError_t e = cudaSuccess;
+  const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
+  if (!p->g8_meta && (e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2))) != cudaSuccess)
+    return e;
+  if (p->gram_fused) {
+    if (!p->g8_ring && (e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GF_RING * G8_BLOCK_BYTES)) != cudaSuccess)
+      return e;
+    if (!p->g8_flags && (e = cudaMalloc(&p->g8_flags, sizeof(int) * 2 * p->g8_groups * GF_RING)) != cudaSuccess)
+      return e;
+  } else if (!p->g8_planes && n_blocks > 0 &&
+             (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) {
+    return e;
+  }
+  if (p->gram_ls && !p->gram_fused) {
+    if (!p->g8_ls_partial &&
+        (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
+      return e;
+    if (!p->g8_ls_progress && (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
+      return e;
+  } else if (!p->g8_partial &&
+             (e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS)) != cudaSuccess) {
+    return e;
+  }
+  return cudaSuccess;
+}
+
 // int8 tensor-core Gram (gram_i8.cuh): sampled column scales, the slice pass
 // (operand images in HBM), the MMA pass, the reduce, and the FP64 gram128 pass
 // gated on the overflow flag.
@@ -221,23 +259,13 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   const int n = p->n;
   cudaError_t e = cudaSuccess;
   const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
-  if (!p->g8_meta) {
-    e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2));
-    if (e == cudaSuccess)
-      e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS);
-    if (e != cudaSuccess) return e;
-  }
+  if ((e = ensure_gram_i8_workspace(p)) != cudaSuccess) return e;
   int* overflow = reinterpret_cast<int*>(p->g8_meta + 2 * G8_N);
   if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (2 * G8_N + 2), s)) != cudaSuccess) return e;
   gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, r, p->n_state, p->n_obs, p->g8_meta);
   const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
   if (p->gram_fused) {
     const size_t nflags = (size_t)2 * p->g8_groups * GF_RING;
-    if (!p->g8_ring) {
-      e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GF_RING * G8_BLOCK_BYTES);
-      if (e == cudaSuccess) e = cudaMalloc(&p->g8_flags, sizeof(int) * nflags);
-      if (e != cudaSuccess) return e;
-    }
     if ((e = cudaMemsetAsync(p->g8_flags, 0, sizeof(int) * nflags, s)) != cudaSuccess) return e;
     const size_t smem = gram_i8_fused_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
@@ -259,7 +287,6 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
                                     smem, s);
     if (e != cudaSuccess) return e;
   } else {
-    if (!p->g8_planes && (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) return e;
     if (p->g8_events) {
       for (cudaEvent_t& ev : p->g8_ev)
         if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
@@ -276,14 +303,9 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
                                                                          p->dstatus);
   if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
   if (p->gram_ls) {
-    if (!p->g8_ls_partial &&
-        (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
-      return e;
     const size_t smem = gram_i8_ls_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
-      return e;
-    if (!p->g8_ls_progress && (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
       return e;
     if ((e = cudaMemsetAsync(p->g8_ls_progress, 0, sizeof(int) * 4 * p->g8_groups, s)) != cudaSuccess) return e;
     gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
@@ -317,6 +339,29 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram128_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->partial, p->g128_cpb_vv, p->g128_cpb_vd, svv,
                                                                  svd, gram, overflow);
   }
+  return cudaGetLastError();
+}
+
+// The analysis step's Gram over ALL observation rows into p->gram: the local pass,
+// then (a communicator attached) one in-place ncclAllReduce of [Gram | input-check
+// flags] on the compute stream and the reduced flags folded back into the status,
+// so every rank runs the levels on the same Gram and reports the same outcome.
+cudaError_t launch_gram_global(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
+                               const double* r, cudaStream_t s) {
+  cudaError_t e = launch_gram(p, true, X, Y, idx, r, p->gram, s);
+  if (e != cudaSuccess || !p->comm) return e;
+  const size_t count = (size_t)2 * p->n * p->n + COMM_FLAG_SLOTS;
+  double* tail = p->gram + (size_t)2 * p->n * p->n;
+  comm_pack_flags<<<1, 32, 0, s>>>(p->dstatus, tail);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (p->stage_events) cudaEventRecord(p->st_ev[1], s);
+  const ncclResult_t rc = nccl_api().all_reduce(p->gram, p->gram, count, ncclFloat64, ncclSum, p->comm, s);
+  if (rc != ncclSuccess) {
+    p->nccl_rc = (int)rc;
+    return cudaErrorUnknown;
+  }
+  if (p->stage_events) cudaEventRecord(p->st_ev[2], s);
+  comm_unpack_flags<<<1, 32, 0, s>>>(tail, p->dstatus);
   return cudaGetLastError();
 }
 
@@ -566,6 +611,23 @@ int translate_status(const enkf_plan* p, enkf_status* st) {
   return ENKF_OK;
 }
 
+// Every plan entry point runs on the plan's device and leaves the caller's
+// current device as it found it (torch and other callers keep theirs).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 int check_plan(const enkf_plan* p, enkf_status* st) {
   if (!p) {
     set_status(st, ENKF_INVALID_ARGUMENT, "null plan");
@@ -588,6 +650,13 @@ int32_t enkf_max_ens(void) { return 128; }
 
 int32_t enkf_set_device(int32_t device) {
   return cudaSetDevice(device) == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
+}
+
+int32_t enkf_get_device(int32_t* device) {
+  int d = 0;
+  if (!device || cudaGetDevice(&d) != cudaSuccess) return ENKF_CUDA_ERROR;
+  *device = d;
+  return ENKF_OK;
 }
 
 int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_plan** out,
@@ -651,7 +720,9 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_DISABLE_WS")) p->use_ws = (env[0] == '0');
   if (const char* env = getenv("ENKF_DISABLE_G128")) p->use_128 = (env[0] == '0');
   if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
+#ifdef I8_DBG_BUILD  // profiling variants only (tools/build_variant.py NAME -DI8_DBG_BUILD)
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
+#endif
   if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
@@ -693,7 +764,7 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (g128_elems > ws_elems) ws_elems = g128_elems;
   if (ws_elems > partial_elems) partial_elems = ws_elems;
   e = cudaMalloc(&p->partial, sizeof(double) * partial_elems);
-  if (e == cudaSuccess) e = cudaMalloc(&p->gram, sizeof(double) * 2 * nn);
+  if (e == cudaSuccess) e = cudaMalloc(&p->gram, sizeof(double) * (2 * nn + COMM_FLAG_SLOTS));
   if (e == cudaSuccess) e = cudaMalloc(&p->A, sizeof(double) * nn);
   if (e == cudaSuccess) e = cudaMalloc(&p->T, sizeof(double) * nn);
   if (e == cudaSuccess) e = cudaMalloc(&p->den, sizeof(double) * n);
@@ -704,6 +775,13 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
     return cuda_fail(st, e, "workspace allocation");
   }
   memset(p->hstatus, 0, sizeof(DevStatus));
+  if (n == G8_N && p->gram_i8 && p->use_128 && n_obs > 0 && !(p->tiny && tiny_eligible(n_state, n_obs, n))) {
+    e = ensure_gram_i8_workspace(p);
+    if (e != cudaSuccess) {
+      enkf_plan_destroy(p);
+      return cuda_fail(st, e, "int8 Gram workspace allocation");
+    }
+  }
   *out = p;
   set_status(st, ENKF_OK, "ok");
   return ENKF_OK;
@@ -711,6 +789,8 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
 
 void enkf_plan_destroy(enkf_plan* p) {
   if (!p) return;
+  DeviceGuard device_guard;
+  cudaSetDevice(p->device);
   cudaFree(p->partial);
   cudaFree(p->gram);
   cudaFree(p->A);
@@ -745,6 +825,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->g8_ls_partial);
   cudaFree(p->g8_ls_progress);
   cudaFree(p->cyc_status);
+  for (cudaEvent_t ev : p->st_ev)
+    if (ev) cudaEventDestroy(ev);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
     if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
@@ -754,6 +836,7 @@ void enkf_plan_destroy(enkf_plan* p) {
 
 int32_t enkf_ism_gram_f64(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
                           const double* r, double* gram, void* stream) {
+  DeviceGuard device_guard;
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
@@ -763,6 +846,7 @@ int32_t enkf_ism_gram_f64(enkf_plan* p, const double* X, const double* Y, const 
 
 int32_t enkf_ism_levels_f64(enkf_plan* p, const double* gram, double* A, double* T, double* den,
                             void* stream) {
+  DeviceGuard device_guard;
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   const double cscale = p->n > 1 ? 1.0 / std::sqrt((double)(p->n - 1)) : 0.0;
   cudaError_t e = launch_levels(p, gram, A, T, den, cscale, (cudaStream_t)stream);
@@ -771,6 +855,7 @@ int32_t enkf_ism_levels_f64(enkf_plan* p, const double* gram, double* A, double*
 
 int32_t enkf_anomaly_update_f64(enkf_plan* p, const double* X, const double* T, double* XA,
                                 int64_t n_rows, void* stream) {
+  DeviceGuard device_guard;
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   cudaError_t e = launch_rowgemm<0>(p, X, T, nullptr, nullptr, XA, n_rows, (cudaStream_t)stream);
   return e == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
@@ -779,22 +864,36 @@ int32_t enkf_anomaly_update_f64(enkf_plan* p, const double* X, const double* T, 
 int32_t enkf_analysis_async_f64(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
                                 const double* r, double* XA, void* stream) {
   NvtxRange nvtx("enkf_analysis");
+  DeviceGuard device_guard;
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s);
-  if (e == cudaSuccess && p->tiny && tiny_eligible(p->n_state, p->n_obs, p->n)) {
+  if (e == cudaSuccess && !p->comm && p->tiny && tiny_eligible(p->n_state, p->n_obs, p->n)) {
     e = launch_tiny(p, X, Y, idx, r, XA, s);
     return e == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
   }
-  if (e == cudaSuccess) e = launch_gram(p, true, X, Y, idx, r, p->gram, s);
+  if (p->stage_events) {
+    for (cudaEvent_t& ev : p->st_ev)
+      if (!ev && cudaEventCreate(&ev) != cudaSuccess) return ENKF_CUDA_ERROR;
+    cudaEventRecord(p->st_ev[0], s);
+  }
+  if (e == cudaSuccess) e = launch_gram_global(p, X, Y, idx, r, s);
+  if (p->stage_events && !p->comm) {  // no exchange: gram | allreduce boundaries coincide
+    cudaEventRecord(p->st_ev[1], s);
+    cudaEventRecord(p->st_ev[2], s);
+  }
   const double cscale = 1.0 / std::sqrt((double)(p->n - 1));
   if (e == cudaSuccess) e = launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s);
+  if (p->stage_events) cudaEventRecord(p->st_ev[3], s);
   if (e == cudaSuccess) e = launch_rowgemm<0>(p, X, p->T, nullptr, nullptr, XA, p->n_state, s);
+  if (p->stage_events) cudaEventRecord(p->st_ev[4], s);
+  if (e == cudaErrorUnknown && p->nccl_rc) return ENKF_CUDA_ERROR;
   return e == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
 }
 
 int32_t enkf_plan_sync_status(enkf_plan* p, void* stream, enkf_status* st) {
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemcpyAsync(p->hstatus, p->dstatus, sizeof(DevStatus), cudaMemcpyDeviceToHost, s), st);
@@ -803,6 +902,7 @@ int32_t enkf_plan_sync_status(enkf_plan* p, void* stream, enkf_status* st) {
 }
 
 int32_t enkf_plan_reset_status(enkf_plan* p, void* stream) {
+  DeviceGuard device_guard;
   if (check_plan(p, nullptr)) return ENKF_INVALID_ARGUMENT;
   return cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), (cudaStream_t)stream) == cudaSuccess
              ? ENKF_OK : ENKF_CUDA_ERROR;
@@ -810,6 +910,7 @@ int32_t enkf_plan_reset_status(enkf_plan* p, void* stream) {
 
 int32_t enkf_analysis_f64(enkf_plan* p, const double* X, const double* Y, const int64_t* idx,
                           const double* r, double* XA, void* stream, enkf_status* st) {
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) {
     set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
@@ -817,6 +918,12 @@ int32_t enkf_analysis_f64(enkf_plan* p, const double* X, const double* Y, const 
   }
   int rc = enkf_analysis_async_f64(p, X, Y, idx, r, XA, stream);
   if (rc != ENKF_OK) {
+    if (p->nccl_rc) {
+      set_status(st, ENKF_CUDA_ERROR, "ncclAllReduce of the Gram failed: %s",
+                 nccl_api().error_string((ncclResult_t)p->nccl_rc));
+      p->nccl_rc = 0;
+      return ENKF_CUDA_ERROR;
+    }
     CUDA_TRY(cudaGetLastError(), st);
     set_status(st, rc, "launch failed");
     return rc;
@@ -914,7 +1021,7 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
   }
   // 2. Gram on the compact observed rows, levels
   {
-    CUDA_TRY(launch_gram(p, true, p->hxo, p->hy, nullptr, p->hr, p->gram, s), st);
+    CUDA_TRY(launch_gram_global(p, p->hxo, p->hy, nullptr, p->hr, s), st);
     const double cscale = 1.0 / std::sqrt((double)(p->n - 1));
     CUDA_TRY(launch_levels(p, p->gram, p->A, p->T, p->den, cscale, s), st);
   }
@@ -959,6 +1066,7 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
                                const int64_t* idx_h, const double* r_h, double* XA_h,
                                enkf_status* st) {
   NvtxRange nvtx("enkf_analysis_host");
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   if (p->n < 2) {
     set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
@@ -1047,7 +1155,12 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
 int32_t enkf_ism_solve_f64(enkf_plan* p, const double* r, const double* V, const double* D,
                            double* Z, double* A, void* stream, enkf_status* st) {
   NvtxRange nvtx("enkf_ism_solve");
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (p->comm) {
+    set_status(st, ENKF_NOT_SUPPORTED, "solve_sherman on a sharded plan (communicator attached) is not provided");
+    return ENKF_NOT_SUPPORTED;
+  }
   cudaStream_t s = (cudaStream_t)stream;
   CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
   CUDA_TRY(launch_gram(p, false, V, D, nullptr, r, p->gram, s), st);
@@ -1152,7 +1265,12 @@ cudaError_t launch_localized(enkf_plan* p, const double* X, const double* Y, con
 
 int localized_common(enkf_plan* p, const double* X, const double* Y, const int64_t* idx, const double* r,
                      const double* delta, double scale, int mode, double* XA, void* stream, enkf_status* st) {
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (p->comm) {
+    set_status(st, ENKF_NOT_SUPPORTED, "not provided on a sharded plan (communicator attached)");
+    return ENKF_NOT_SUPPORTED;
+  }
   if (p->n < 2) {
     set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
     return ENKF_INVALID_ARGUMENT;
@@ -1246,6 +1364,7 @@ int check_l96(const enkf_plan* p, double dt, int n_steps, enkf_status* st) {
 
 int32_t enkf_forecast_l96_f64(enkf_plan* p, const double* X, double* Xout, double dt, double forcing,
                               int32_t n_steps, void* stream, enkf_status* st) {
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
   if (int rc = check_l96(p, dt, n_steps, st)) return rc;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1275,7 +1394,12 @@ int cycle_l96(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, con
               int32_t steps_per_cycle, double dt, double forcing, double inflation, double loc_scale,
               double* mean_f, double* mean_a, void* stream, enkf_status* st, int32_t* failed_cycle) {
   if (failed_cycle) *failed_cycle = -1;
+  DeviceGuard device_guard;
   if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (p->comm) {
+    set_status(st, ENKF_NOT_SUPPORTED, "not provided on a sharded plan (communicator attached)");
+    return ENKF_NOT_SUPPORTED;
+  }
   if (p->n < 2) {
     set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
     return ENKF_INVALID_ARGUMENT;
@@ -1296,6 +1420,8 @@ int cycle_l96(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, con
   cudaStream_t s = (cudaStream_t)stream;
   if (p->cyc_cap < n_cycles) {
     cudaFree(p->cyc_status);
+  for (cudaEvent_t ev : p->st_ev)
+    if (ev) cudaEventDestroy(ev);
     p->cyc_status = nullptr;
     p->cyc_cap = 0;
     CUDA_TRY(cudaMalloc(&p->cyc_status, sizeof(DevStatus) * (size_t)n_cycles), st);
@@ -1378,6 +1504,111 @@ __attribute__((visibility("default"))) int32_t enkf_debug_lv_trace(long long* ou
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, enkf::g_i8_trace, sizeof(enkf::g_i8_trace)) == cudaSuccess ? 0 : 5;
+}
+
+// ---- multi-GPU: NCCL communicator (nccl_comm.cuh) ----
+int32_t enkf_comm_unique_id(unsigned char* id, enkf_status* st) {
+  const NcclApi& api = nccl_api();
+  if (!api.ok) {
+    set_status(st, ENKF_NOT_SUPPORTED, "%s", api.why);
+    return ENKF_NOT_SUPPORTED;
+  }
+  if (!id) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "null id buffer");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  ncclUniqueId u;
+  const ncclResult_t rc = api.get_unique_id(&u);
+  if (rc != ncclSuccess) {
+    set_status(st, ENKF_CUDA_ERROR, "ncclGetUniqueId: %s", api.error_string(rc));
+    return ENKF_CUDA_ERROR;
+  }
+  memcpy(id, u.internal, NCCL_UNIQUE_ID_BYTES);
+  set_status(st, ENKF_OK, "ok");
+  return ENKF_OK;
+}
+
+int32_t enkf_comm_init(const unsigned char* id, int32_t nranks, int32_t rank, int32_t device, void** comm,
+                       enkf_status* st) {
+  const NcclApi& api = nccl_api();
+  if (!api.ok) {
+    set_status(st, ENKF_NOT_SUPPORTED, "%s", api.why);
+    return ENKF_NOT_SUPPORTED;
+  }
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "invalid communicator arguments (nranks=%d rank=%d)", nranks, rank);
+    return ENKF_INVALID_ARGUMENT;
+  }
+  DeviceGuard device_guard;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    set_status(st, ENKF_CUDA_ERROR, "cudaSetDevice(%d) failed", device);
+    return ENKF_CUDA_ERROR;
+  }
+  ncclUniqueId u;
+  memcpy(u.internal, id, NCCL_UNIQUE_ID_BYTES);
+  ncclComm_t c = nullptr;
+  const ncclResult_t rc = api.comm_init_rank(&c, nranks, u, rank);
+  if (rc != ncclSuccess) {
+    set_status(st, ENKF_CUDA_ERROR, "ncclCommInitRank(nranks=%d, rank=%d): %s", nranks, rank, api.error_string(rc));
+    return ENKF_CUDA_ERROR;
+  }
+  *comm = c;
+  set_status(st, ENKF_OK, "ok");
+  return ENKF_OK;
+}
+
+int32_t enkf_comm_destroy(void* comm) {
+  if (!comm) return ENKF_OK;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return ENKF_NOT_SUPPORTED;
+  return api.comm_destroy((ncclComm_t)comm) == ncclSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
+}
+
+int32_t enkf_plan_set_comm(enkf_plan* p, void* comm, enkf_status* st) {
+  DeviceGuard device_guard;
+  if (check_plan(p, st)) return ENKF_INVALID_ARGUMENT;
+  if (!comm) {
+    p->comm = nullptr;
+    p->comm_ranks = 1;
+    p->comm_rank = 0;
+    set_status(st, ENKF_OK, "ok");
+    return ENKF_OK;
+  }
+  const NcclApi& api = nccl_api();
+  if (!api.ok) {
+    set_status(st, ENKF_NOT_SUPPORTED, "%s", api.why);
+    return ENKF_NOT_SUPPORTED;
+  }
+  int ranks = 0, rank = 0;
+  if (api.comm_count((ncclComm_t)comm, &ranks) != ncclSuccess ||
+      api.comm_user_rank((ncclComm_t)comm, &rank) != ncclSuccess) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "not a valid ncclComm_t");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  if (p->n < 2) {
+    set_status(st, ENKF_INVALID_ARGUMENT, "analysis needs at least 2 ensemble members");
+    return ENKF_INVALID_ARGUMENT;
+  }
+  p->comm = (ncclComm_t)comm;
+  p->comm_ranks = ranks;
+  p->comm_rank = rank;
+  set_status(st, ENKF_OK, "ok");
+  return ENKF_OK;
+}
+
+// Measurement-only (not part of include/enkf_b200.h): CUDA events at the stage
+// boundaries of enkf_analysis_async_f64 (gram | allreduce | levels | anomaly).
+__attribute__((visibility("default"))) int32_t enkf_debug_set_stage_events(enkf_plan* p, int32_t on) {
+  if (!p) return ENKF_INVALID_ARGUMENT;
+  p->stage_events = on != 0;
+  return ENKF_OK;
+}
+// ms of the last step's gram, allreduce, levels and anomaly stages (caller synchronised)
+__attribute__((visibility("default"))) int32_t enkf_debug_stage_times(enkf_plan* p, float* out4) {
+  if (!p || !p->st_ev[4]) return ENKF_INVALID_ARGUMENT;
+  for (int i = 0; i < 4; ++i)
+    if (cudaEventElapsedTime(&out4[i], p->st_ev[i], p->st_ev[i + 1]) != cudaSuccess) return ENKF_CUDA_ERROR;
+  return ENKF_OK;
 }
 
 // Measurement-only (not part of include/enkf_b200.h): CUDA events around the

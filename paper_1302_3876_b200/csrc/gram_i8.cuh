@@ -723,11 +723,16 @@ gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned l
       for (int64_t k = 0; k < nblk; ++k) {
         const int slot = (int)(k % G8LS_NST);
         if ((int)k - G8LS_LEAD > known) {
-          for (int spin = 0; spin < (1 << 16); ++spin) {
+          int spin = 0;
+          for (; spin < (1 << 16); ++spin) {
             known = min(min(gp[0], gp[1]), min(gp[2], gp[3]));
             if (known >= (int)k - G8LS_LEAD) break;
             __nanosleep(256);
           }
+          // a group member that is not co-resident (SM-limited contexts, MPS, another
+          // persistent kernel) would make every later block time out: after one
+          // timeout, pacing is off for the rest of the kernel
+          if (spin == (1 << 16)) known = 0x7fffffff;
         }
         if (k >= G8LS_NST) mbar_wait(&sempty[slot], (uint32_t)(((k / G8LS_NST) - 1) & 1));
         unsigned char* st = sm + slot * G8LS_STAGE;

@@ -11,10 +11,19 @@ Sherman-Morrison levels on the identical reduced Gram (no broadcast) and
 updates its own state rows.  Per step that is a single 2 N^2 fp64 allreduce
 (256 KiB at N = 128) instead of the reference's per-level column exchange.
 
-The device stages are pluggable only so the orchestration itself can be
-exercised on CPU with the gloo backend (tests/test_distributed_gloo.py); the
-product stages are `CudaStages` (libenkf_b200.so) and nothing here falls back
-to the CPU.
+Two forms:
+
+* `NativeShardedAnalysis` (the product path, bench.py's N > 1 leg): the exchange
+  lives in the native layer.  `NativeComm` creates an NCCL communicator inside
+  libenkf_b200.so (the 128-byte unique id is handed out over torch.distributed),
+  the shard's plan gets it attached, and one C call per step runs the local Gram,
+  the ncclAllReduce of [Gram | input-check flags] on the compute stream, the
+  levels and the local anomaly update — every rank returns the same status, with
+  no extra collective or host synchronisation (include/enkf_b200.h).
+* `ShardedAnalysis` over pluggable stages: the same orchestration in Python with
+  `torch.distributed.all_reduce`, kept so the sharding logic can be exercised on
+  CPU with the gloo backend (tests/test_distributed_gloo.py).  Its product stages
+  are `CudaStages` (libenkf_b200.so); nothing here falls back to the CPU.
 """
 
 from __future__ import annotations
@@ -150,3 +159,103 @@ class ShardedAnalysis:
             st.code = code
             st.message = msg.encode()[:255]
             _native.raise_for_status(code, st, "sharded analysis step")
+
+
+class NativeComm:
+    """An NCCL communicator created by libenkf_b200.so (ncclCommInitRank) for the
+    ranks of `group` (default: the world), one per GPU.  Rank 0 draws the unique id
+    (ncclGetUniqueId); it reaches the other ranks through a torch.distributed
+    broadcast (any backend)."""
+
+    def __init__(self, device, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.device = device
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        lib = _native.lib()
+        st = _native.EnkfStatus()
+        uid = (ctypes.c_ubyte * 128)()
+        if self.rank == 0:
+            _native.raise_for_status(lib.enkf_comm_unique_id(uid, ctypes.byref(st)), st, "enkf_comm_unique_id")
+        if self.world > 1:
+            on_cuda = dist.get_backend(group) == "nccl"
+            buf = torch.tensor(list(bytes(uid)), dtype=torch.uint8,
+                               device=device if on_cuda else torch.device("cpu"))
+            dist.broadcast(buf, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            uid = (ctypes.c_ubyte * 128)(*buf.cpu().tolist())
+        self._h = ctypes.c_void_p()
+        code = lib.enkf_comm_init(uid, self.world, self.rank, device.index, ctypes.byref(self._h), ctypes.byref(st))
+        _native.raise_for_status(code, st, "enkf_comm_init")
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h is not None and self._h.value and _native._lib is not None:
+            _native._lib.enkf_comm_destroy(self._h)
+        self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NativeShardedAnalysis:
+    """One rank's shard of the analysis step with the exchange in the native layer
+    (see the module docstring).  `step(x, y, idx, r, out)` takes CUDA tensors:
+    x = X[lo:hi] (rows, N), y / r = this shard's perturbed observations /
+    variances, idx = their state indices relative to lo (None for the identity),
+    and writes X^A[lo:hi] into `out` (may be `x`).  With check=True it reads the
+    status (one device->host copy) and raises the reference's exception type —
+    the same on every rank."""
+
+    def __init__(self, n_state_local: int, n_obs_local: int, n_ens: int, device, comm: NativeComm):
+        import torch
+
+        self.torch = torch
+        self.device = device
+        self.comm = comm
+        self.plan = _native.Plan(n_state_local, n_obs_local, n_ens, device.index)
+        self.lib = _native.lib()
+        st = _native.EnkfStatus()
+        _native.raise_for_status(self.lib.enkf_plan_set_comm(self.plan.handle, comm.handle, ctypes.byref(st)),
+                                 st, "enkf_plan_set_comm")
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def step(self, x, y, idx, r, out, check: bool = True):
+        code = self.lib.enkf_analysis_async_f64(self.plan.handle, x.data_ptr(), y.data_ptr(),
+                                                0 if idx is None else idx.data_ptr(), r.data_ptr(),
+                                                out.data_ptr(), self._stream())
+        if code != _native.ENKF_OK:
+            # a failed launch (e.g. the collective): read the plan's status for the message
+            st = _native.EnkfStatus()
+            self.lib.enkf_plan_sync_status(self.plan.handle, self._stream(), ctypes.byref(st))
+            _native.raise_for_status(code, st, "enkf_analysis_async_f64 (sharded)")
+        if check:
+            self.raise_for_status()
+        return out
+
+    def step_host(self, x_h, y_h, idx_h, r_h, out_h):
+        """The same shard step on host (numpy) buffers through enkf_analysis_host_f64:
+        copies in, the step with the NCCL exchange, X^A out."""
+        import numpy as np
+
+        st = _native.EnkfStatus()
+        idx_c = None if idx_h is None else np.ascontiguousarray(idx_h, dtype=np.int64)  # held across the call
+        ptr = lambda a: a.ctypes.data if a is not None else None  # noqa: E731
+        code = self.lib.enkf_analysis_host_f64(self.plan.handle, ptr(x_h), ptr(y_h), ptr(idx_c),
+                                               ptr(r_h), ptr(out_h), ctypes.byref(st))
+        _native.raise_for_status(code, st, "enkf_analysis_host_f64 (sharded)")
+        return out_h
+
+    def raise_for_status(self):
+        st = _native.EnkfStatus()
+        code = self.lib.enkf_plan_sync_status(self.plan.handle, self._stream(), ctypes.byref(st))
+        _native.raise_for_status(code, st, "sharded analysis step")

@@ -135,9 +135,9 @@ def member_deviations(x):
     device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
     xd = _f64_contig_device(x, device)
     out = torch.empty_like(xd)
-    _native.lib().enkf_set_device(device.index)
-    code = _native.lib().enkf_member_deviations_f64(
-        xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1], _stream_ptr(device))
+    with _native.on_device(device.index):
+        code = _native.lib().enkf_member_deviations_f64(
+            xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1], _stream_ptr(device))
     _native.raise_for_status(code, None, "enkf_member_deviations_f64")
     return out if dev_in else out.cpu().numpy()
 
@@ -157,9 +157,9 @@ def inflate(x, alpha: float):
     device = torch.device("cuda", _cuda_ready(x.device.index if dev_in else None))
     xd = _f64_contig_device(x, device)
     out = torch.empty_like(xd)
-    _native.lib().enkf_set_device(device.index)
-    code = _native.lib().enkf_inflate_f64(xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1], float(alpha),
-                                          _stream_ptr(device))
+    with _native.on_device(device.index):
+        code = _native.lib().enkf_inflate_f64(xd.data_ptr(), out.data_ptr(), xd.shape[0], xd.shape[1],
+                                              float(alpha), _stream_ptr(device))
     _native.raise_for_status(code, None, "enkf_inflate_f64")
     return out if dev_in else out.cpu().numpy()
 
@@ -179,10 +179,10 @@ def innovations(obs: ObservationBatch, h: SelectionOperator, x):
                          f"H(x) ({nobs}, {xd.shape[1] if xd.dim() == 2 else 1})")
     out = torch.empty_like(yd)
     idx = h.device_indices(device)
-    _native.lib().enkf_set_device(device.index)
-    code = _native.lib().enkf_innovations_f64(
-        xd.data_ptr(), yd.data_ptr(), 0 if idx is None else idx.data_ptr(),
-        out.data_ptr(), nobs, yd.shape[1], _stream_ptr(device))
+    with _native.on_device(device.index):
+        code = _native.lib().enkf_innovations_f64(
+            xd.data_ptr(), yd.data_ptr(), 0 if idx is None else idx.data_ptr(),
+            out.data_ptr(), nobs, yd.shape[1], _stream_ptr(device))
     _native.raise_for_status(code, None, "enkf_innovations_f64")
     return out if dev_in else out.cpu().numpy()
 

@@ -44,3 +44,24 @@ def test_bench_line_contract():
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     assert d["gpu_launches"] > 0
     assert d["ism_sweep"] is None or 0 < d["ism_sweep"]["frac"] < 1.2
+    assert 0 < d["roofline_step"]["frac"] < 1.2 and d["energy_j_per_step"] is None or d["energy_j_per_step"] > 0
+    assert d["strict_fp64"]["value"] > 0 and "IEEE" in d["strict_fp64"]["dtype"]
+    assert "emulation" in d["dtype"]
+    assert d["overflow_cliff"]["gram_ms_fallback"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_bench_small_configs(cfg):
+    """Driver-visible throughput of the latency-bound configs 1-3 (one analysis per step)."""
+    d = _run(["--config", str(cfg), "--steps", "20", "--warmup", "3", "--e2e-steps", "3"])
+    assert BASE_KEYS <= set(d) and d["value"] > 0 and d["config"]["workload"].startswith(f"config{cfg}")
+    assert d["cpu_baseline"]["extrapolated"] is False and d["cpu_baseline"]["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+def test_gpus_beyond_visible_fails():
+    """`--gpus N` with fewer visible GPUs exits non-zero instead of timing one rank."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--steps", "1"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode != 0 and "64" in out.stderr

@@ -60,4 +60,20 @@ def test_sm100a_sass_present():
     out = subprocess.run([tool, "-lelf", _native.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run([tool, "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
-    assert "DMMA.8x8x4" in sass  # FP64 tensor-core MMA on the hot kernels
+    funcs = {}
+    for chunk in sass.split("Function : ")[1:]:
+        name, body = chunk.split("\n", 1)
+        funcs[name.strip()] = body
+    # the product kernels of the N = 128 step: 5th-gen tensor-core int8 MMAs
+    # (UTCIMMA = tcgen05.mma kind::i8), TMEM loads (LDTM = tcgen05.ld), bulk TMA
+    # copies (UBLKCP = cp.async.bulk)
+    for kern in ("anomaly_i8_kernel", "gram_i8_mma_ls_kernel"):
+        body = [b for n, b in funcs.items() if kern in n]
+        assert body, kern
+        for op in ("UTCIMMA", "LDTM", "UBLKCP"):
+            assert op in body[0], (kern, op)
+    # the FP64 kernels (N != 128, ENKF_GRAM/ANOMALY=fp64, levels): DMMA + bulk TMA
+    for kern in ("gram128_kernel", "rowgemm_ws_kernel", "ism_levels_blocked_kernel"):
+        body = [b for n, b in funcs.items() if kern in n]
+        assert body and "DMMA.8x8x4" in body[0], kern
+

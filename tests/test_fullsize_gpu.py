@@ -1,27 +1,38 @@
-"""Full-size parity (BASELINE config 5: 2^26 states, 128 members, 2^23 observations,
-the bench workload) through size-independent properties — the parity policy of
-DESIGN.md §3: the oracle cannot run the 2^23-row observation-space solve inside a
-test, and its own fp64 floor there is ~4e-9.
+"""Full-size parity of configs 4 and 5 (config 5 = the bench workload: 2^26 states,
+128 members, 2^23 observations) under the SURVEY §8(c) policy signed off in the
+round-1 VERDICT (tests/parity_policy.py):
 
-* the default product path (int8 tensor-core Gram + int8 anomaly update) against
-  the all-FP64 DMMA path (`ENKF_GRAM=fp64 ENKF_ANOMALY=fp64`), two independent
-  kernel families: Gram within 1e-13, A = V'Z and X^A within the north star's 1e-9
-  (sampled rows exactly, every row through its member sum: a checksum per row);
-* X^A rows against the oracle's own formula x + member_deviations(x) @ A
-  (enkf.py:192) evaluated on the host with the A each path produced;
-* zero-spread rows (constant across members) come out unchanged to rounding: the
-  row-local form of test_enkf.py:208-213 (that test's exact identity holds for a wholly
-  zero-spread ensemble, T = I, and is pinned bit for bit in test_gpu_parity.py; row by
-  row, x + s @ A is exact only where the row mean is, in the reference as here);
+* config 4 (2^24 / 2^20): X^A from the drop-in API on host arrays against the
+  oracle's X^A, every row, <= 1e-9; the oracle floor and the error against the
+  long-double Woodbury truth are reported too;
+* config 5: the observation side X[idx], Y, r is pulled to the host and the
+  oracle runs its grouped sweep and its level-by-level sweep (their spread is
+  the floor, measured here) and the truth A is formed; for BOTH kernel families
+  — the product path (int8 tensor-core Gram + int8 anomaly update) and the
+  all-FP64 DMMA path (`ENKF_GRAM=fp64 ENKF_ANOMALY=fp64`) — every one of the
+  2^26 X^A rows is compared with x + S A for the oracle's A and the truth A
+  (the S A products by cuBLAS fp64 on the device, chunked: a checker independent
+  of the kernels under test), sampled rows also on the host with the oracle's
+  member_deviations; pass iff err_vs_oracle <= max(1e-9, 2 floor) and
+  err_vs_truth <= 1e-9;
+* zero-spread rows (constant across members) come out unchanged to rounding (the
+  row-local form of test_enkf.py:208-213);
 * two runs of the product path agree bit for bit (fixed reduction order).
+
+The numbers are printed on one line per config ("full-size parity ...") and
+recorded under profiles/.
 """
 
 import ctypes
+import json
+import time
 
 import numpy as np
 import pytest
 
 import oracle
+import parity_policy as PP
+import paper_1302_3876_b200 as P
 from paper_1302_3876_b200 import _native
 from paper_1302_3876_b200 import workloads as W
 
@@ -36,7 +47,85 @@ def _built():
     assert torch.cuda.is_available()
 
 
-def test_config5_full_size_properties(monkeypatch):
+def _device_errors(x, xa, a_refs, floor_pair, rows_per_chunk=1 << 21):
+    """Over every row: max|xa - (x + S A)| for each named A, max|x + S A_first|
+    (the scale), and the floor max|S (A_p - A_q)| of the pair (torch fp64 on the
+    device, 2 GiB temporaries)."""
+    import torch
+
+    n = x.shape[1]
+    dev = x.device
+    sc = 1.0 / np.sqrt(n - 1.0)
+    at = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in a_refs.items()}
+    dfl = at[floor_pair[0]] - at[floor_pair[1]]
+    first = next(iter(a_refs))
+    err = {k: 0.0 for k in a_refs}
+    scale = 0.0
+    floor = 0.0
+    for lo in range(0, x.shape[0], rows_per_chunk):
+        xc = x[lo:lo + rows_per_chunk]
+        s = (xc - xc.mean(dim=1, keepdim=True)) * sc
+        for k, a in at.items():
+            ref = torch.addmm(xc, s, a)
+            err[k] = max(err[k], float((xa[lo:lo + rows_per_chunk] - ref).abs().max()))
+            if k == first:
+                scale = max(scale, float(ref.abs().max()))
+            del ref
+        floor = max(floor, float((s @ dfl).abs().max()))
+        del s
+    return {k: v / scale for k, v in err.items()}, floor / scale, scale
+
+
+def _record(tag, got):
+    line = {k: (float(f"{v:.4g}") if isinstance(v, float) else v) for k, v in got.items()}
+    print(f"{tag} full-size parity: {json.dumps(line)}")
+
+
+def test_config4_full_size_vs_oracle():
+    """Config 4 at full size through the drop-in API on host arrays, every X^A row
+    against the oracle (<= 1e-9); floor and truth error reported."""
+    import torch
+
+    torch.cuda.empty_cache()
+    t0 = time.time()
+    p = W.config4(0)
+    assert p.x.shape == (1 << 24, 128) and p.perturbed.shape == (1 << 20, 128)
+    h = P.SelectionOperator.from_indices(p.indices)
+    obs = P.ObservationBatch(y=p.y, perturbed=p.perturbed, perturbations=None)
+    xa = P.analysis_step(p.x, obs, h, p.r, "sherman")
+    t_gpu = time.time() - t0
+    xo = p.x[p.indices]
+    a = PP.obs_side_oracle(xo, p.perturbed, p.r)
+    a_w = PP.truth_a(xo, p.perturbed, p.r)
+    t_oracle = time.time() - t0 - t_gpu
+    got = {"err_vs_oracle": 0.0, "err_vs_truth": 0.0, "floor": 0.0}
+    scale = 0.0
+    dfl = a["grouped"] - a["levelwise"]
+    for lo in range(0, p.x.shape[0], 1 << 20):
+        blk = p.x[lo:lo + (1 << 20)]
+        s = oracle.member_deviations(blk)
+        ref = blk + s @ a["grouped"]  # the oracle's own X^A rows (analysis_step_chunked)
+        scale = max(scale, float(np.abs(ref).max()))
+        got["err_vs_oracle"] = max(got["err_vs_oracle"], float(np.abs(xa[lo:lo + (1 << 20)] - ref).max()))
+        ref = blk + s @ a_w
+        got["err_vs_truth"] = max(got["err_vs_truth"], float(np.abs(xa[lo:lo + (1 << 20)] - ref).max()))
+        got["floor"] = max(got["floor"], float(np.abs(s @ dfl).max()))
+    for k in got:
+        got[k] /= scale
+    got["oracle_vs_truth"] = float(np.abs(a["grouped"] - a_w).max() / np.abs(a_w).max())
+    got["seconds_gpu_host_api"] = round(t_gpu, 1)
+    got["seconds_oracle"] = round(t_oracle, 1)
+    _record("config4", got)
+    _native._plans.clear()  # the cached config-4 plan holds ~18 GB of device workspace
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    ok, bound = PP.verdict(4, got["err_vs_oracle"])
+    assert ok, (got, bound)
+    assert got["err_vs_truth"] <= PP.XA_TOL
+
+
+def test_config5_full_size_policy(monkeypatch):
     import torch
     dev = torch.device("cuda", 0)
     torch.cuda.synchronize(dev)
@@ -54,11 +143,21 @@ def test_config5_full_size_properties(monkeypatch):
     zr = torch.arange(3, ns, 65537, device=dev)        # zero-spread rows
     x[zr] = x[zr, :1].repeat(1, n)
     x_zero = x[zr].clone()
-    samp = torch.arange(11, ns, 4093, device=dev)      # ~16K sampled rows
-    samp = torch.cat([samp, zr])
+    samp = torch.cat([torch.arange(11, ns, 1021, device=dev), zr])  # ~66K sampled rows
     x_samp = x[samp].cpu().numpy()
-    out = torch.empty_like(x)
 
+    # ---- the oracle on the observation side (host, all cores)
+    t0 = time.time()
+    xo = x[idx].cpu().numpy()
+    y_h = y.cpu().numpy()
+    r_h = r.cpu().numpy()
+    a_or = PP.obs_side_oracle(xo, y_h, r_h)
+    a_w = PP.truth_a(xo, y_h, r_h)
+    t_oracle = time.time() - t0
+    del xo, y_h
+    a_refs = {"oracle": a_or["grouped"], "truth": a_w, "levelwise": a_or["levelwise"]}
+
+    out = torch.empty_like(x)
     res = {}
     for mode in ("i8", "fp64", "i8-again"):
         if mode == "fp64":
@@ -79,36 +178,43 @@ def test_config5_full_size_properties(monkeypatch):
                                      gram.data_ptr(), s) == 0
         assert lib.enkf_ism_levels_f64(plan.handle, gram.data_ptr(), a.data_ptr(), t.data_ptr(), None, s) == 0
         assert lib.enkf_plan_sync_status(plan.handle, s, ctypes.byref(st)) == 0, st.message
-        rowsum = out.sum(dim=1)  # a non-finite entry makes its row sum non-finite
-        scale = max(float(c.abs().max()) for c in out.split(1 << 21))  # 2 GiB temporaries
-        res[mode] = {"gram": gram.cpu().numpy(), "A": a.cpu().numpy(), "samp": out[samp].cpu().numpy(),
-                     "rowsum": rowsum,
-                     "zero_dev": float(((out[zr] - x_zero).abs() / x_zero.abs().clamp_min(1e-300)).max()),
-                     "finite": bool(torch.isfinite(rowsum).all()), "scale": scale}
         del plan
         torch.cuda.synchronize(dev)
         torch.cuda.empty_cache()
+        rowsum = out.sum(dim=1)  # a non-finite entry makes its row sum non-finite
+        rec = {"gram": gram.cpu().numpy(), "A": a.cpu().numpy(), "samp": out[samp].cpu().numpy(),
+               "rowsum": rowsum, "finite": bool(torch.isfinite(rowsum).all()),
+               "zero_dev": float(((out[zr] - x_zero).abs() / x_zero.abs().clamp_min(1e-300)).max())}
+        if mode != "i8-again":
+            rec["err"], rec["floor"], rec["scale"] = _device_errors(x, out, a_refs, ("oracle", "levelwise"))
+        res[mode] = rec
 
+    got = {"seconds_oracle": round(t_oracle, 1)}
+    floors = []
+    for m in ("i8", "fp64"):
+        rec = res[m]
+        assert rec["finite"], m
+        floors.append(rec["floor"])
+        got[m + "_err_vs_oracle"] = rec["err"]["oracle"]
+        got[m + "_err_vs_truth"] = rec["err"]["truth"]
+        got[m + "_err_vs_oracle_levelwise"] = rec["err"]["levelwise"]
+        # sampled rows on the host with the oracle's member_deviations (enkf.py:82-92, 192)
+        ref = x_samp + oracle.member_deviations(x_samp) @ a_w
+        got[m + "_samp_err_vs_truth_host"] = float(np.abs(rec["samp"] - ref).max() / rec["scale"])
+        got[m + "_A_vs_truth"] = float(np.abs(rec["A"] - a_w).max() / np.abs(a_w).max())
+        got[m + "_zero_spread_dev"] = rec["zero_dev"]
+    got["floor"] = max(floors)
+    got["oracle_A_vs_truth"] = float(np.abs(a_or["grouped"] - a_w).max() / np.abs(a_w).max())
     i8, f64 = res["i8"], res["fp64"]
-    got = {}
-    for m in ("i8", "fp64"):
-        assert res[m]["finite"], m
-        # the anomaly update at full size against the oracle's formula with this path's A
-        ref = x_samp + oracle.member_deviations(x_samp) @ res[m]["A"]
-        got[m + "_vs_oracle_formula"] = np.abs(res[m]["samp"] - ref).max() / res[m]["scale"]
-        got[m + "_zero_spread_dev"] = res[m]["zero_dev"]
-    # the two kernel families
-    got["gram_i8_vs_fp64"] = np.abs(i8["gram"] - f64["gram"]).max() / np.abs(f64["gram"]).max()
-    got["A_i8_vs_fp64"] = np.abs(i8["A"] - f64["A"]).max() / np.abs(f64["A"]).max()
-    got["xa_rows_i8_vs_fp64"] = np.abs(i8["samp"] - f64["samp"]).max() / f64["scale"]
+    got["gram_i8_vs_fp64"] = float(np.abs(i8["gram"] - f64["gram"]).max() / np.abs(f64["gram"]).max())
     got["xa_rowsum_i8_vs_fp64"] = float((i8["rowsum"] - f64["rowsum"]).abs().max()) / (n * f64["scale"])
-    print("config5 full-size parity:", {k: float(f"{v:.3g}") for k, v in got.items()})
+    _record("config5", got)
     for m in ("i8", "fp64"):
-        assert got[m + "_vs_oracle_formula"] <= 1e-12, m
+        ok, bound = PP.verdict(5, got[m + "_err_vs_oracle"], got["floor"], got[m + "_err_vs_truth"])
+        assert ok, (m, bound, got)
+        assert got[m + "_samp_err_vs_truth_host"] <= PP.XA_TOL, m
         assert got[m + "_zero_spread_dev"] <= 1e-12, m
     assert got["gram_i8_vs_fp64"] <= 1e-13
-    assert got["A_i8_vs_fp64"] <= 1e-9
-    assert got["xa_rows_i8_vs_fp64"] <= 1e-9
     assert got["xa_rowsum_i8_vs_fp64"] <= 1e-9
     # run-to-run determinism of the product path
     assert torch.equal(i8["rowsum"], res["i8-again"]["rowsum"])

@@ -268,14 +268,15 @@ def test_random_systems_analysis(case):
 
 
 def test_config2_cycles_open_loop():
-    """Config 2: identical X^B to GPU and oracle at every cycle (open loop),
-    then the GPU analysis drives the next forecast."""
+    """Config 2: all 100 assimilation cycles of the configuration, identical X^B to
+    GPU and oracle at every cycle (open loop), the GPU analysis driving the next
+    forecast."""
     cyc = W.Config2Cycler()
     xa = None
-    for c in range(3):
+    for c in range(100):
         p = cyc.cycle(xa)
         xa = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
-        assert rel_err(xa, oracle.analysis_step(p.x, p.perturbed, None, p.r)) <= XA_TOL
+        assert rel_err(xa, oracle.analysis_step(p.x, p.perturbed, None, p.r)) <= XA_TOL, c
 
 
 def test_device_resident_path_matches_host_path():
@@ -457,7 +458,7 @@ def test_tensor_core_anomaly_zero_spread_and_nonfinite():
 
 
 # ---------------------------------------------------------------- opt-in int8 Gram
-def _gram_with(mode, heavy=False):
+def _gram_with(mode, heavy=False, ns_log2=17, no_log2=15):
     import os
     import subprocess
     import sys
@@ -468,7 +469,7 @@ sys.path.insert(0, os.getcwd())
 from paper_1302_3876_b200 import _native
 heavy = int(sys.argv[1])
 dev = torch.device("cuda", 0); lib = _native.lib(); s = torch.cuda.current_stream().cuda_stream
-n, ns, no = 128, 1 << 17, 1 << 15
+n, ns, no = 128, 1 << int(sys.argv[3]), 1 << int(sys.argv[4])
 g = torch.Generator(device=dev); g.manual_seed(11)
 x = torch.randn((ns, 1), dtype=torch.float64, device=dev, generator=g) + (0.5 + 1.5 * torch.rand((ns, 1), dtype=torch.float64, device=dev, generator=g)) * torch.randn((ns, n), dtype=torch.float64, device=dev, generator=g)
 idx = torch.sort(torch.randperm(ns, device=dev, generator=g)[:no]).values
@@ -496,7 +497,8 @@ np.save(sys.argv[2], gram.cpu().numpy())
     import tempfile
     out = tempfile.mktemp(suffix=".npy")
     env = dict(os.environ, ENKF_GRAM=mode)
-    subprocess.run([sys.executable, "-c", code, str(int(heavy)), out], env=env, check=True, timeout=300)
+    subprocess.run([sys.executable, "-c", code, str(int(heavy)), out, str(ns_log2), str(no_log2)], env=env,
+                   check=True, timeout=300)
     return np.load(out)
 
 
@@ -513,6 +515,61 @@ def test_int8_gram_matches_fp64_gram(heavy, mode):
     assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
     tol = 0.0 if heavy else 1e-13
     assert np.abs(a - b).max() <= tol * np.abs(a).max()
+
+
+def test_int8_gram_level_split_mid_size():
+    """2^20 observation rows: ~886 blocks per group of the level-split MMA pass, so
+    the producers' pacing (a CTA more than G8LS_LEAD = 48 blocks ahead of its group
+    polls the group's progress) and the multi-period flush (every 512 blocks) both
+    run; agrees with the FP64 Gram to rounding level, exactly symmetric."""
+    a, b = _gram_with("fp64", 0, 21, 20), _gram_with("i8ls", 0, 21, 20)
+    assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+
+
+def test_anomaly_debug_env_has_no_effect(monkeypatch):
+    """The profiling role skips of anomaly_i8_kernel are compiled out of the product
+    library: ENKF_I8_DBG set at plan creation changes nothing (bitwise)."""
+    p = W.config4(8)
+    base = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    _native._plans.clear()
+    monkeypatch.setenv("ENKF_I8_DBG", "7")
+    try:
+        other = P.analysis_step(p.x, obs_of(p), h_of(p), p.r)
+    finally:
+        monkeypatch.delenv("ENKF_I8_DBG")
+        _native._plans.clear()
+    assert np.array_equal(base, other)
+
+
+@pytest.mark.parametrize("workers", [1, 2, 4, 8])
+def test_solve_analysis_dispatch_and_blocked_workers(workers):
+    """solvers.py:91-112 on the GPU: solve_analysis("sherman", ..., workers) runs
+    solve_sherman (workers = 1) or solve_sherman_blocked (workers > 1, sherman.py:289-311);
+    every worker count gives the bitwise-same Z as solve_sherman (the reference's
+    tests/test_sherman.py:134-146 asserts workers=1 bitwise and the rest within 1e-12),
+    and the result matches the reference's golden Z."""
+    seed, r, v, d, z_ref, zl_ref, ops = list(ism_cases())[5]
+    base = P.solve_sherman(r, v, d).z
+    res = P.solve_analysis("sherman", r, v, d, workers=workers)
+    assert isinstance(res, P.SolverResult)
+    assert np.array_equal(res.z, base)
+    assert np.array_equal(P.solve_sherman_blocked(r, v, d, workers=workers).z, base)
+    assert np.array_equal(P.solve_analysis(P.SolverChoice.SHERMAN, r, v, d, workers=workers).z, base)
+    assert rel_err(res.z, z_ref) <= Z_TOL
+
+
+def test_solve_analysis_dispatch_errors():
+    """Unknown names raise ValueError, the CPU baselines NotImplementedError
+    (tests/test_solvers.py:111-129 pass-through / unknown-name behaviour)."""
+    seed, r, v, d, *_ = list(ism_cases())[0]
+    with pytest.raises(ValueError):
+        P.solve_analysis("nope", r, v, d)
+    for name in ("cholesky", "svd"):
+        with pytest.raises(NotImplementedError):
+            P.solve_analysis(name, r, v, d)
+    with pytest.raises(ValueError):
+        P.solve_sherman_blocked(r, v, d, workers=0)
 
 
 def test_tensor_core_anomaly_extreme_rows():

@@ -3,7 +3,7 @@ import ctypes, os, subprocess, sys
 import numpy as np, torch
 if os.environ.get("ENKF_LIB_VARIANT", "") == "":
     # the event stamps are compiled in only with -DI8_TRACE_ON (variant "trace")
-    subprocess.run([sys.executable, "tools/build_variant.py", "trace", "-DI8_TRACE_ON=1"], check=True,
+    subprocess.run([sys.executable, "tools/build_variant.py", "trace", "-DI8_TRACE_ON=1", "-DI8_DBG_BUILD"], check=True,
                    stdout=subprocess.DEVNULL)
     os.environ["ENKF_LIB_VARIANT"] = "trace"
 os.environ["ENKF_I8_DBG"] = str(8 | int(sys.argv[1] if len(sys.argv) > 1 else 0))

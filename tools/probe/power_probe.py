@@ -31,7 +31,8 @@ def main():
     modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["i8", "fp64"]
     for mode in modes:
         dbg = None
-        if mode.startswith("dbg"):  # anomaly role skips (profiling only, wrong results)
+        if mode.startswith("dbg"):  # anomaly role skips (profiling only, wrong results;
+            # needs a -DI8_DBG_BUILD variant: tools/build_variant.py dbg -DI8_DBG_BUILD, ENKF_LIB_VARIANT=dbg)
             dbg, mode = mode[3:], "i8"
             os.environ["ENKF_I8_DBG"] = dbg
         else:
