@@ -143,7 +143,10 @@ def nccl_init_lines(d):
 
 # ----------------------------------------------------------------------------- CPU legs
 def cpu_sample_log2(cfg: int, scale: int) -> int:
-    return {4: 6, 5: 8}[cfg] - scale if cfg in (4, 5) else 0
+    """The smaller of the two CPU samples (the larger is 4x its rows): config 5 at
+    1/64 and 1/16 (the 1/256 sample is dominated by per-level Python overhead: 4x the
+    rows took only 2.3x the time on the box), config 4 at 1/16 and 1/4."""
+    return {4: 4, 5: 6}[cfg] - scale if cfg in (4, 5) else 0
 
 
 def _threads():
@@ -250,6 +253,38 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows),
                 "power_w": statistics.median(pw) if pw else None}
+
+
+class EnergyMeter:
+    """Board energy over a region from NVML's cumulative counter
+    (nvmlDeviceGetTotalEnergyConsumption, mJ); None where unavailable."""
+
+    def __init__(self, index):
+        self.index = index
+        self.joules = None
+        self._h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self._h = None
+
+    def _read(self):
+        try:
+            return float(self._nv.nvmlDeviceGetTotalEnergyConsumption(self._h)) / 1e3
+        except Exception:
+            return None
+
+    def __enter__(self):
+        self._e0 = self._read() if self._h is not None else None
+        return self
+
+    def __exit__(self, *a):
+        if self._e0 is not None:
+            e1 = self._read()
+            self.joules = (e1 - self._e0) if e1 is not None else None
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -411,7 +446,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     runner.check(sptr)
-    with ClockSampler(local) as clocks:
+    with ClockSampler(local) as clocks, EnergyMeter(local) as energy:
         ms = timed_steps(step, args.steps, dev, stream, world, dist)
     runner.check(sptr)
     sync = lambda: torch.cuda.synchronize(dev)  # noqa: E731
@@ -439,7 +474,7 @@ def run_ours(args):
         for _ in range(max(1, args.warmup)):
             step64()
         r64.check(sptr)
-        with ClockSampler(local) as clocks64:
+        with ClockSampler(local) as clocks64, EnergyMeter(local) as energy64:
             ms64 = timed_steps(step64, args.steps, dev, stream, world, dist)
         r64.check(sptr)
         st64 = r64.stage_times(step64, sync)
@@ -447,7 +482,7 @@ def run_ours(args):
         strict = {"value": args.steps / (ms64 / 1e3), "unit": "steps/s", "ms_per_step": ms64 / args.steps,
                   "dtype": "f64 (IEEE: FP64 DMMA m8n8k4 Gram + FP64 DMMA anomaly update)",
                   "kernels_ms": st64, "clocks": cs,
-                  "energy_j_per_step": (cs["power_w"] * ms64 / args.steps / 1e3) if cs.get("power_w") else None,
+                  "energy_j_per_step": energy64.joules / args.steps if energy64.joules else None,
                   "env": "ENKF_GRAM=fp64 ENKF_ANOMALY=fp64"}
         del r64
 
@@ -638,8 +673,11 @@ def run_ours(args):
         "strict_fp64": strict,
         "overflow_cliff": cliff,
         "clocks": {k: cs[k] for k in ("sm_mhz", "sm_max_mhz", "reasons", "samples")},
-        "power_w": cs.get("power_w"),
-        "energy_j_per_step": (cs["power_w"] * ms_step / 1e3) if cs.get("power_w") else None,
+        # board energy of the timed region from NVML's cumulative counter (this GPU);
+        # the step runs at the ~1 kW power cap, so J/step is what bounds steps/s
+        "energy_j_per_step": energy.joules / args.steps if energy.joules else None,
+        "power_w": energy.joules / (ms / 1e3) if energy.joules else None,
+        "energy_scope": "rank 0's GPU board (NVML total-energy counter over the timed region)",
         "gpu_launches": per_step * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,

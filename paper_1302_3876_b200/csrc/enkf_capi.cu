@@ -229,20 +229,21 @@ cudaError_t ensure_gram_i8_workspace(enkf_plan* p) {
   const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
   if (!p->g8_meta && (e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2))) != cudaSuccess)
     return e;
-  if (p->gram_fused) {
-    if (!p->g8_ring && (e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GF_RING * G8_BLOCK_BYTES)) != cudaSuccess)
+  if (p->gram_fused) {  // L2-resident per-group image rings + their ready / consumed counters
+    if (!p->g8_ring && (e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GFL_RING * G8LS_STAGE)) != cudaSuccess)
       return e;
-    if (!p->g8_flags && (e = cudaMalloc(&p->g8_flags, sizeof(int) * 2 * p->g8_groups * GF_RING)) != cudaSuccess)
+    if (!p->g8_flags && (e = cudaMalloc(&p->g8_flags, sizeof(int) * 2 * p->g8_groups * GFL_RING)) != cudaSuccess)
       return e;
   } else if (!p->g8_planes && n_blocks > 0 &&
              (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) {
     return e;
   }
-  if (p->gram_ls && !p->gram_fused) {
+  if (p->gram_ls || p->gram_fused) {
     if (!p->g8_ls_partial &&
         (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
       return e;
-    if (!p->g8_ls_progress && (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
+    if (!p->gram_fused && !p->g8_ls_progress &&
+        (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
       return e;
   } else if (!p->g8_partial &&
              (e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS)) != cudaSuccess) {
@@ -265,27 +266,33 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, r, p->n_state, p->n_obs, p->g8_meta);
   const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
   if (p->gram_fused) {
-    const size_t nflags = (size_t)2 * p->g8_groups * GF_RING;
+    const size_t nflags = (size_t)2 * p->g8_groups * GFL_RING;
     if ((e = cudaMemsetAsync(p->g8_flags, 0, sizeof(int) * nflags, s)) != cudaSuccess) return e;
     const size_t smem = gram_i8_fused_smem_bytes();
     if ((e = cudaFuncSetAttribute(gram_i8_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
       return e;
     int* ready = p->g8_flags;
-    int* consumed = p->g8_flags + (size_t)p->g8_groups * GF_RING;
+    int* consumed = p->g8_flags + (size_t)p->g8_groups * GFL_RING;
     int64_t n_state = p->n_state, n_obs = p->n_obs, nb = n_blocks, bpg_v = bpg;
     const unsigned long long* cmax = p->g8_meta;
-    double* partial = p->g8_partial;
+    double* partial = p->g8_ls_partial;
     DevStatus* dstatus = p->dstatus;
     unsigned char* ring = p->g8_ring;
-    uint32_t uz = 0;
     void* args[] = {(void*)&X, (void*)&Y, (void*)&idx, (void*)&r, (void*)&cmax, (void*)&n_state, (void*)&n_obs,
                     (void*)&nb, (void*)&bpg_v, (void*)&ring, (void*)&ready, (void*)&consumed, (void*)&partial,
-                    (void*)&overflow, (void*)&dstatus, (void*)&uz};
+                    (void*)&overflow, (void*)&dstatus};
+    if (p->g8_events) {
+      for (cudaEvent_t& ev : p->g8_ev)
+        if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
+      cudaEventRecord(p->g8_ev[0], s);
+      cudaEventRecord(p->g8_ev[1], s);
+    }
     // cooperative: every CTA co-resident (they wait on each other through the ring)
-    e = cudaLaunchCooperativeKernel((const void*)gram_i8_fused_kernel, dim3(4 * p->g8_groups), dim3(GF_THREADS), args,
-                                    smem, s);
+    e = cudaLaunchCooperativeKernel((const void*)gram_i8_fused_kernel, dim3(4 * p->g8_groups), dim3(GFL_THREADS),
+                                    args, smem, s);
     if (e != cudaSuccess) return e;
+    if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   } else {
     if (p->g8_events) {
       for (cudaEvent_t& ev : p->g8_ev)
@@ -321,7 +328,7 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
-  if (p->gram_ls && !p->gram_fused)
+  if (p->gram_ls || p->gram_fused)
     gram_i8_ls_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_ls_partial, p->g8_groups, svv, svd, overflow,
                                                                     gram);
   else

@@ -527,6 +527,18 @@ def test_int8_gram_level_split_mid_size():
     assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
 
 
+@pytest.mark.parametrize("sizes", [(17, 15), (21, 20), (17, 10)])
+def test_fused_gram_equals_two_kernel_gram(sizes):
+    """The one-kernel Gram (slicers and level-split MMAs on the same SMs, images
+    through an L2-resident ring) performs the same exact digit products in the same
+    order as the two-kernel form: the two Grams are identical bit for bit (2^15 rows:
+    < 1 block per CTA; 2^20: multi-period flush, ring wrap; 2^13: groups without
+    blocks)."""
+    a = _gram_with("i8ls", 0, *sizes)
+    b = _gram_with("i8fused", 0, *sizes)
+    assert np.array_equal(a, b)
+
+
 def test_anomaly_debug_env_has_no_effect(monkeypatch):
     """The profiling role skips of anomaly_i8_kernel are compiled out of the product
     library: ENKF_I8_DBG set at plan creation changes nothing (bitwise)."""
