@@ -44,7 +44,6 @@ struct enkf_plan {
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
   bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
-  bool gram_ls = true;                    // level-split N = 256 MMA pass (default; ENKF_GRAM=i8: column split)
   double* g8_ls_partial = nullptr;        // [groups][4][256][128] (level-split form)
   int* g8_ls_progress = nullptr;          // [groups][4] blocks issued per CTA (level-split pacing)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
@@ -57,7 +56,6 @@ struct enkf_plan {
   unsigned char* g8_ring = nullptr;       // [groups][GF_RING][48 KiB] L2-resident image ring (fused form)
   int* g8_flags = nullptr;                // [2][groups][GF_RING] ready / consumed counters
   unsigned long long* g8_meta = nullptr;  // [256] sampled column maxima, then the overflow flag
-  double* g8_partial = nullptr;           // [groups][4][128][64]
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
   int g128_cpb_vv = 1, g128_cpb_vd = 1;     // gram128: CTAs for the V'V / V'D blocks
@@ -238,17 +236,12 @@ cudaError_t ensure_gram_i8_workspace(enkf_plan* p) {
              (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) {
     return e;
   }
-  if (p->gram_ls || p->gram_fused) {
-    if (!p->g8_ls_partial &&
-        (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
-      return e;
-    if (!p->gram_fused && !p->g8_ls_progress &&
-        (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
-      return e;
-  } else if (!p->g8_partial &&
-             (e = cudaMalloc(&p->g8_partial, sizeof(double) * (size_t)p->g8_groups * 4 * G8_N * G8_NS)) != cudaSuccess) {
+  if (!p->g8_ls_partial &&
+      (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
     return e;
-  }
+  if (!p->gram_fused && !p->g8_ls_progress &&
+      (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
+    return e;
   return cudaSuccess;
 }
 
@@ -308,31 +301,19 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
                                                                          p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                          p->dstatus);
-  if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
-  if (p->gram_ls) {
-    const size_t smem = gram_i8_ls_smem_bytes();
-    if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+    if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
+    const size_t lsmem = gram_i8_ls_smem_bytes();
+    if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem)) !=
         cudaSuccess)
       return e;
     if ((e = cudaMemsetAsync(p->g8_ls_progress, 0, sizeof(int) * 4 * p->g8_groups, s)) != cudaSuccess) return e;
-    gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
-                                                                       p->g8_ls_partial, overflow, p->g8_ls_progress);
-  } else {
-    const size_t smem = gram_i8_smem_bytes();
-    if ((e = cudaFuncSetAttribute(gram_i8_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    gram_i8_mma_kernel<<<4 * p->g8_groups, G8_THREADS, smem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
-                                                                  p->g8_partial, overflow, 0u);
-  }
-  if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
+    gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, lsmem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
+                                                                        p->g8_ls_partial, overflow, p->g8_ls_progress);
+    if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   }
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
-  if (p->gram_ls || p->gram_fused)
-    gram_i8_ls_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_ls_partial, p->g8_groups, svv, svd, overflow,
-                                                                    gram);
-  else
-    gram_i8_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_partial, p->g8_groups, svv, svd, overflow, gram);
+  gram_i8_ls_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_ls_partial, p->g8_groups, svv, svd, overflow,
+                                                                  gram);
   // FP64 fallback, a no-op unless an element fell outside the sampled scales
   {
     const int ld = padded_ld(W_TILE);
@@ -734,7 +715,6 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
     p->gram_fused = (strcmp(env, "i8fused") == 0);
-    p->gram_ls = (strcmp(env, "i8") != 0);  // ENKF_GRAM=i8: the column-split MMA pass
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
@@ -828,7 +808,6 @@ void enkf_plan_destroy(enkf_plan* p) {
     if (ev) cudaEventDestroy(ev);
   cudaFree(p->g8_flags);
   cudaFree(p->g8_meta);
-  cudaFree(p->g8_partial);
   cudaFree(p->g8_ls_partial);
   cudaFree(p->g8_ls_progress);
   cudaFree(p->cyc_status);
@@ -1509,6 +1488,9 @@ __attribute__((visibility("default"))) int32_t enkf_debug_lv_trace(long long* ou
 }
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
+__attribute__((visibility("default"))) int32_t enkf_debug_gfl_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, enkf::g_gfl_trace, sizeof(enkf::g_gfl_trace)) == cudaSuccess ? 0 : 5;
+}
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, enkf::g_i8_trace, sizeof(enkf::g_i8_trace)) == cudaSuccess ? 0 : 5;
 }

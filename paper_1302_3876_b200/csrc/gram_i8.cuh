@@ -15,15 +15,15 @@
 //    images: per block, [P planes 6 x 4 KiB | Q planes 6 x 4 KiB], each plane
 //    128 members x 32 K-bytes, K-major with the 32-byte swizzle.  An element
 //    outside its column scale (heavy tail, non-finite) raises the overflow flag.
-//  * gram_i8_mma_kernel (tensor-bound): pure TMA -> tcgen05 pipeline.  CTAs come
-//    in groups of 4 over the same observation blocks; CTA q owns 64 output
-//    columns: q = 0,1 -> P'P[:, 64q..] (B operand = a 2 KiB slice of the A planes
-//    already in shared memory), q = 2,3 -> P'Q[:, 64(q-2)..] (B = 6 x 2 KiB of Q
-//    planes).  26 digit pairs (p + q <= 8) per 32-row block accumulate per level
-//    l = p + q in 7 TMEM accumulators of 64 columns; every 512 blocks (16384
-//    rows, where the int32 levels are still exact) 4 flush warps fold the levels
-//    into the fp64 partial.  No FP64 arithmetic runs next to the MMAs (on B200 it
-//    stalls the tensor pipe, anomaly_i8.cuh).
+//  * gram_i8_mma_ls_kernel (the MMA pass): pure TMA -> tcgen05 pipeline.  CTAs come
+//    in groups of 4 over the same observation blocks and split the 26 digit pairs
+//    (p + q <= 8) by level l = p + q: each owns all 256 output columns [P'P | P'Q] for
+//    two levels (two 256-column int32 accumulators = all of TMEM) and issues one
+//    N = 256 kind::i8 MMA per pair with A = P_p and B = [P_q ; Q_q] from shared memory;
+//    every 512 blocks (16384 rows, where the int32 levels are still exact) 4 flush
+//    warps fold the levels into the fp64 partial.  No FP64 arithmetic runs next to the
+//    MMAs (on B200 it stalls the tensor pipe, anomaly_i8.cuh).
+// gram_i8_fused.cuh holds an opt-in one-kernel form of the same products.
 // Any overflow -> the FP64 DMMA Gram (gram128_kernel, gated on the flag, same
 // stream) recomputes the Gram: no host round trip, same results contract.
 #pragma once
@@ -33,29 +33,12 @@
 namespace enkf {
 
 constexpr int G8_N = 128;
-constexpr int G8_NS = 64;        // output columns per CTA
 constexpr int G8_KB = 32;        // observation rows per digit block (one MMA k-step)
 constexpr int G8_ND = 6;         // digits per value
-#ifndef G8_LMAX_DEF
-#define G8_LMAX_DEF 8
-#endif
-constexpr int G8_LMAX = G8_LMAX_DEF;  // pairs p + q <= G8_LMAX (1-based digit index)
-constexpr int G8_NLEV = G8_LMAX - 1;
+// digit pairs p + q <= 8 (1-based digit index): 26 pairs, levels 2..8 (g8ls_level)
 constexpr int G8_FLUSH_BLOCKS = 512;  // 16384 rows per int32 accumulation period
 constexpr int G8_PLANE = G8_N * G8_KB;            // 4 KiB: one plane, 128 members x 32 B
 constexpr int G8_BLOCK_BYTES = 2 * G8_ND * G8_PLANE;  // 48 KiB per 32-row block (P and Q)
-constexpr int G8_BSL = G8_NS * G8_KB;             // 2 KiB: a 64-member slice of a plane
-constexpr int G8_STAGE = G8_ND * G8_PLANE + G8_ND * G8_BSL;  // 36 KiB: A planes + B slices
-constexpr int G8_NST = 5;        // stage ring depth
-constexpr int G8_THREADS = 6 * 32;  // producer, MMA issuer, 4 flush warps
-#ifndef G8_MMA_ONLY
-#define G8_MMA_ONLY 0            // profiling only: MMAs on the first stages' data, no streaming
-#endif
-#ifndef G8_TS
-#define G8_TS 1                  // A operand (P digit planes) from TMEM (tcgen05.cp), B from smem
-#endif
-constexpr int G8_ATM = G8_NLEV * G8_NS;  // TMEM column of the A planes (after the level accumulators)
-static_assert(G8_ATM + 8 * G8_ND <= 512, "TMEM: accumulators + A planes");
 constexpr int G8_SAMPLE = 16;    // pre-pass samples every 16th observation row at least ...
 constexpr int64_t G8_SAMPLES_MAX = 1 << 17;  // ... and at most ~128K rows (sparser for large n_obs)
 __host__ __device__ inline int64_t g8_sample_stride(int64_t n_obs) {
@@ -70,9 +53,6 @@ constexpr int G8_SLICE_THREADS = 256;
 #endif
 constexpr int G8_VLD = 2 * G8_N + 1;  // slice-kernel staging row stride (uint64)
 
-__host__ __device__ inline size_t gram_i8_smem_bytes() {
-  return 1024 + (size_t)G8_NST * G8_STAGE + 64 * 8 /*barriers*/;
-}
 __host__ __device__ inline size_t gram_i8_slice_smem_bytes() {
   return (size_t)G8_KB * G8_VLD * 8 + 2 * G8_N * 8 /*scales*/;
 }
@@ -87,10 +67,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw32(uint32_t smem_addr) {
   d |= (uint64_t)6 << 61;  // SWIZZLE_32B
   return d;
 }
-// kind::i8, D = s32, both operands signed (balanced digits), K-major, M = 128, N = 64
-__device__ __forceinline__ uint32_t idesc_g8() {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(G8_NS >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-}
 __device__ __forceinline__ void umma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
@@ -104,204 +80,10 @@ __device__ __forceinline__ void umma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uin
       : "memory");
 }
 
-// The same issue sequence as one PTX block (G8_TS): one elect for the 6 copies
-// and 26 MMAs of a block; generated for G8_ND = 6, G8_LMAX = 8, G8_ATM = 448.
-__device__ __forceinline__ void g8_issue_block_asm(uint32_t uz, uint64_t a0, uint64_t b0, uint64_t bst16,
-                                                   uint32_t acc_first) {
-  asm volatile(
-        "{\n"
-        ".reg .pred e, pa, pt;\n"
-        ".reg .b64 ad, bd;\n"
-        ".reg .b32 dt, at;\n"
-        "elect.sync _|e, 0xffffffff;\n"
-        "setp.ne.b32 pa, %3, 0;\n"
-        "setp.eq.b32 pt, %4, %4;\n"
-        "add.u64 ad, %0, 0;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "add.u64 ad, %0, 256;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "add.u64 ad, %0, 512;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "add.u64 ad, %0, 768;\n"
-        "add.u32 at, %4, 472;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "add.u64 ad, %0, 1024;\n"
-        "add.u32 at, %4, 480;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "add.u64 ad, %0, 1280;\n"
-        "add.u32 at, %4, 488;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [at], ad;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 0;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 64;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 2, %1;\n"
-        "add.u32 dt, %4, 128;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 3, %1;\n"
-        "add.u32 dt, %4, 192;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 4, %1;\n"
-        "add.u32 dt, %4, 256;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 5, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 448;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 64;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 128;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 2, %1;\n"
-        "add.u32 dt, %4, 192;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 3, %1;\n"
-        "add.u32 dt, %4, 256;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 4, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 5, %1;\n"
-        "add.u32 dt, %4, 384;\n"
-        "add.u32 at, %4, 456;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pa;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 128;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 192;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 2, %1;\n"
-        "add.u32 dt, %4, 256;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 3, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 4, %1;\n"
-        "add.u32 dt, %4, 384;\n"
-        "add.u32 at, %4, 464;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 192;\n"
-        "add.u32 at, %4, 472;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 256;\n"
-        "add.u32 at, %4, 472;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 2, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 472;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 3, %1;\n"
-        "add.u32 dt, %4, 384;\n"
-        "add.u32 at, %4, 472;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 256;\n"
-        "add.u32 at, %4, 480;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 480;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 2, %1;\n"
-        "add.u32 dt, %4, 384;\n"
-        "add.u32 at, %4, 480;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 0, %1;\n"
-        "add.u32 dt, %4, 320;\n"
-        "add.u32 at, %4, 488;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "mad.lo.u64 bd, %2, 1, %1;\n"
-        "add.u32 dt, %4, 384;\n"
-        "add.u32 at, %4, 488;\n"
-        "@e tcgen05.mma.cta_group::1.kind::i8 [dt], [at], bd, %5, pt;\n"
-        "}\n"
-        ::"l"(a0), "l"(b0), "l"(bst16), "r"(acc_first), "r"(uz), "r"(uz + idesc_g8())
-        : "memory");
-}
-
-// Issue one 32-row block: the six A planes smem -> TMEM (columns G8_ATM + 8(p-1);
-// tcgen05.cp and tcgen05.mma from one thread execute in issue order, so the copy
-// waits for the previous block's MMAs and the MMAs see the copy — shared-memory
-// reads per block drop from 26 x 6 KiB (SS operands) to 24 + 26 x 2 KiB) and the
-// digit-pair MMAs into the level accumulators (columns 64(l-2)).  TMEM addresses
-// are compile-time offsets from `uz` (a kernel parameter equal to 0: the CTA owns
-// all 512 columns, so its allocation starts at column 0) and the descriptors are
-// one base per operand plus constants, so the operands stay on the uniform datapath.
-__device__ __forceinline__ void g8_issue_block(uint32_t uz, uint32_t abuf, uint32_t bbuf, uint32_t bstride,
-                                               bool first_in_period) {
-  const uint64_t a0 = umma_desc_sw32(abuf);
-  const uint64_t b0 = umma_desc_sw32(bbuf);
-#if G8_TS && G8_LMAX_DEF == 8
-  static_assert(G8_ND == 6 && G8_NS == 64 && G8_ATM == 448, "g8_issue_block_asm is generated for this shape");
-  g8_issue_block_asm(uz, a0, b0, (uint64_t)(bstride >> 4), first_in_period ? 0u : 1u);
-  return;
-#endif
-  const uint32_t idesc = uz + idesc_g8();
-#if G8_TS
-#pragma unroll
-  for (int p = 0; p < G8_ND; ++p)
-    asm volatile(
-        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
-        "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n}\n" ::"r"(uz + (uint32_t)(G8_ATM + 8 * p)),
-        "l"(a0 + (uint64_t)((p * G8_PLANE) >> 4))
-        : "memory");
-#endif
-#pragma unroll
-  for (int p = 1; p <= G8_ND; ++p) {
-#pragma unroll
-    for (int qq = 1; qq <= G8_ND; ++qq) {
-      if (p + qq > G8_LMAX) continue;
-      const int l = p + qq;
-      const bool first = first_in_period && ((p == 1) || (l > G8_ND + 1 && p == l - G8_ND));
-      const uint64_t bd = b0 + (uint64_t)(((uint32_t)(qq - 1) * bstride) >> 4);
-#if G8_TS
-      umma_i8_ts(uz + (uint32_t)((l - 2) * G8_NS), uz + (uint32_t)(G8_ATM + 8 * (p - 1)), bd, idesc,
-                 first ? 0u : 1u);
-#else
-      umma_i8_ss(uz + (uint32_t)((l - 2) * G8_NS), a0 + (uint64_t)(((p - 1) * G8_PLANE) >> 4), bd, idesc,
-                 first ? 0u : 1u);
-#endif
-    }
-  }
-}
-
 // 2^(47 - e - headroom) for a column whose sampled max|.| has IEEE bits b
 __device__ __forceinline__ double g8_scale(unsigned long long b) { return pow2(47 - exp_above(b) - G8_HEADROOM); }
 
 __device__ __forceinline__ double g8_sqrt_rho(double rv) { return sqrt(1.0 / rv); }
-
-// sum_l acc_l 256^(8-l) over the kept levels l = 2..G8_LMAX (v[l-2][c]), in units of
-// 256^0 at level 8: exact products, smallest level first
-__device__ __forceinline__ double g8_combine(const uint32_t (&v)[G8_NLEV][8], int c) {
-  double s = 0.0;
-#pragma unroll
-  for (int l = G8_NLEV - 1; l >= 0; --l) s = fma((double)(int)v[l][c], pow2(8 * (6 - l)), s);
-  return s;
-}
 
 // Column maxima over every g8_sample_stride(n_obs)-th observation row (16th, or
 // sparser so that ~128K rows are sampled): |P| (128) then |Q| (128),
@@ -514,140 +296,16 @@ gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y,
 }
 
 // ---------------------------------------------------------------------------
-// MMA pass: warp 0 producer (bulk TMA of the ready-made operand images), warp 1
-// MMA issuer (owns TMEM), warps 2-5 flush (TMEM lane quadrants).
-__global__ void __launch_bounds__(G8_THREADS, 1)
-gram_i8_mma_kernel(const unsigned char* __restrict__ planes, const unsigned long long* __restrict__ cmax,
-                   int64_t n_blocks, int64_t blocks_per_group, double* __restrict__ partial,
-                   const int* __restrict__ overflow, uint32_t uz /* = 0 */) {
-  if (*overflow) return;  // the FP64 fallback computes the Gram
-  extern __shared__ __align__(1024) unsigned char g8sm_raw[];
-  unsigned char* sm = g8sm_raw + ((1024u - (smem_u32(g8sm_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + G8_NST * G8_STAGE);
-  uint64_t* sfull = bars;              // [NST] producer -> MMA (tx)
-  uint64_t* sempty = bars + G8_NST;    // [NST] MMA commit -> producer
-  uint64_t* afull = bars + 2 * G8_NST; // MMA commit -> flush
-  uint64_t* aempty = afull + 1;        // flush -> MMA
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 1);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = blockIdx.x & 3;
-  const int64_t grp = blockIdx.x >> 2;
-  const int64_t b0 = grp * blocks_per_group;
-  const int64_t b1 = b0 + blocks_per_group < n_blocks ? b0 + blocks_per_group : n_blocks;
-  const int64_t nblk = b1 > b0 ? b1 - b0 : 0;
-  const bool qslice = q >= 2;
-
-  if (tid == 0) {
-    for (int i = 0; i < G8_NST; ++i) {
-      mbar_init(&sfull[i], 1);
-      mbar_init(&sempty[i], 1);
-    }
-    mbar_init(afull, 1);
-    mbar_init(aempty, 128);  // the 4 flush warps
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512u)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  constexpr uint32_t tmem = 0;  // one CTA per SM owns all 512 columns
-  if (tid == 0 && *tmem_slot != 0u) __trap();
-
-  if (warp == 0) {
-    // ---- producer ---------------------------------------------------------------
-    if (lane == 0) {
-      const uint32_t bytes = (uint32_t)(G8_ND * G8_PLANE + (qslice ? G8_ND * G8_BSL : 0));
-      for (int64_t k = 0; k < (G8_MMA_ONLY ? (nblk < G8_NST ? nblk : G8_NST) : nblk); ++k) {
-        const int slot = (int)(k % G8_NST);
-        if (k >= G8_NST) mbar_wait(&sempty[slot], (uint32_t)(((k / G8_NST) - 1) & 1));
-        unsigned char* st = sm + slot * G8_STAGE;
-        const unsigned char* src = planes + (size_t)(b0 + k) * G8_BLOCK_BYTES;
-        mbar_arrive_expect_tx(&sfull[slot], bytes);
-        bulk_g2s(st, src, (uint32_t)(G8_ND * G8_PLANE), &sfull[slot]);
-        if (qslice) {
-#pragma unroll
-          for (int p = 0; p < G8_ND; ++p)
-            bulk_g2s(st + G8_ND * G8_PLANE + p * G8_BSL,
-                     src + G8_ND * G8_PLANE + p * G8_PLANE + (q - 2) * G8_BSL, (uint32_t)G8_BSL, &sfull[slot]);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---- MMA issuer ---------------------------------------------------------------
-    const uint32_t sbase = smem_u32(sm);
-    for (int64_t k = 0; k < nblk; ++k) {
-      const int slot = (int)(k % G8_NST);
-      const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
-      if (first_in_period && k > 0) mbar_wait(aempty, (uint32_t)(((k / G8_FLUSH_BLOCKS) - 1) & 1));
-      if (!G8_MMA_ONLY || k < G8_NST) mbar_wait(&sfull[slot], (uint32_t)((k / G8_NST) & 1));
-      tc_fence_after();
-      const uint32_t abuf = sbase + (uint32_t)(slot * G8_STAGE);
-      // B: a 64-member slice of the A planes (P'P) or the Q slices (P'Q)
-      const uint32_t bbuf = qslice ? abuf + (uint32_t)(G8_ND * G8_PLANE) : abuf + (uint32_t)(q * G8_BSL);
-      const uint32_t bstride = qslice ? (uint32_t)G8_BSL : (uint32_t)G8_PLANE;
-      g8_issue_block(uz, abuf, bbuf, bstride, first_in_period);
-      umma_commit_elect(&sempty[slot]);
-      if ((k % G8_FLUSH_BLOCKS) == G8_FLUSH_BLOCKS - 1 || k == nblk - 1) umma_commit_elect(afull);
-      __syncwarp();
-    }
-  } else {
-    // ---- flush: thread = member i = TMEM lane; fold the 7 levels into the fp64 partial
-    const int quad = warp & 3;  // warps 2..5 -> quadrants 2,3,0,1 (TMEM lane access is warp % 4)
-    const int i = 32 * quad + lane;
-    const int64_t nper = (nblk + G8_FLUSH_BLOCKS - 1) / G8_FLUSH_BLOCKS;
-    double* prow = partial + ((size_t)blockIdx.x * G8_N + i) * G8_NS;
-    // Gamma_ij = 2^(e_i + f_j - 94) sum_l 256^(12-l) D_l = (hi 2^32 + lo) 2^(e_i+f_j-62),
-    // and 2^(47-e) = sc  ->  2^(e_i+f_j-62) = 2^32 / (sc_i sc_j)
-    const double ai = 4294967296.0 / g8_scale(cmax[i]);
-    const unsigned long long* bmax = cmax + (qslice ? G8_N + 64 * (q - 2) : 64 * q);
-    double acc[G8_NS];
-#pragma unroll
-    for (int j = 0; j < G8_NS; ++j) acc[j] = 0.0;
-    for (int64_t pd = 0; pd < nper; ++pd) {
-      mbar_wait(afull, (uint32_t)(pd & 1));
-      tc_fence_after();
-#pragma unroll
-      for (int cg = 0; cg < G8_NS / 8; ++cg) {
-        uint32_t v[G8_NLEV][8];
-#pragma unroll
-        for (int l = 0; l < G8_NLEV; ++l)
-          tmem_ld8(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(l * G8_NS + 8 * cg), v[l]);
-        tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          acc[8 * cg + c] += g8_combine(v, c);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(aempty);
-    }
-#pragma unroll
-    for (int j = 0; j < G8_NS; ++j) prow[j] = acc[j] * (ai / g8_scale(bmax[j]));
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512u) : "memory");
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Level-split MMA pass (default; ENKF_GRAM=i8 selects the column-split
-// gram_i8_mma_kernel above).  The 4 CTAs of a group split the
+// Level-split MMA pass (the product MMA pass; an earlier column-split form with
+// N = 64 MMAs and A in TMEM was measured slower and removed).  The 4 CTAs
+// of a group split the
 // digit pairs by level l = p + q instead of by output column: CTA r owns the level
 // set G8LS_SETS[r] ({7}, {8, 2}, {6, 3}, {5, 4}: 6, 6, 7, 7 pairs) for all 256
 // output columns [P'P | P'Q], in two 256-column int32 accumulators (all of TMEM).
 // Each pair is ONE N = 256 MMA with A = P_p and B = [P_q ; Q_q] straight from
 // shared memory (the producer lays each block's planes out as P_1 Q_1 P_2 Q_2 ...,
 // so one 256-row K-major descriptor spans P_q and Q_q): no tcgen05.cp, 4x the math
-// per instruction of the column split (tools/probe/g8_levelsplit_probe.cu: N = 256
+// per instruction of a column split (tools/probe/g8_levelsplit_probe.cu: N = 256
 // from shared memory runs at the 128-cycle math floor).  The flush folds the CTA's
 // two levels into its fp64 partial [group][r][256 columns][128 members]
 // (read-modify-write in global memory, coalesced across a warp's members);
@@ -801,7 +459,8 @@ gram_i8_mma_ls_kernel(const unsigned char* __restrict__ planes, const unsigned l
       tc_fence_before();
       mbar_arrive(aempty);
     }
-    // scales: 2^(e_i + f_j - 62) = 2^32 / (sc_i sc_j)  (see gram_i8_mma_kernel)
+    // scales: 2^(e_i + f_j - 62) = 2^32 / (sc_i sc_j): each operand carries 2^(47 - e - 2),
+    // the level weights are in units of level 8 = 2^-62 of the combined scale
     const double ai = 4294967296.0 / g8_scale(cmax[i]);
     for (int j = 0; j < 2 * G8_N; ++j) prow[(size_t)j * G8_N] *= ai / g8_scale(cmax[j]);
   }
@@ -828,31 +487,6 @@ __global__ void gram_i8_ls_reduce(const double* __restrict__ partial, int ngroup
   for (int g = 0; g < ngroups; ++g)
 #pragma unroll
     for (int rr = 0; rr < 4; ++rr) s += src[((size_t)g * 4 + rr) * G8_N * 2 * G8_N];
-  gram[e] = s * (c < G8_N ? s_vv : s_vd);
-}
-
-// Gram from the per-CTA partials [group][quarter][128][64]: fixed-order sum over
-// groups; the V'V block from its upper triangle (exactly symmetric); scales
-// s_vv = 1/(N-1), s_vd = 1/sqrt(N-1).  Skipped when the FP64 fallback ran.
-__global__ void gram_i8_reduce(const double* __restrict__ partial, int ngroups, double s_vv, double s_vd,
-                               const int* __restrict__ overflow, double* __restrict__ gram) {
-  if (*overflow) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= G8_N * 2 * G8_N) return;
-  const int i = e / (2 * G8_N), c = e % (2 * G8_N);
-  int qq, a, b;
-  if (c < G8_N) {
-    a = i <= c ? i : c;
-    b = i <= c ? c : i;
-    qq = b >> 6;
-  } else {
-    a = i;
-    b = c - G8_N;
-    qq = 2 + (b >> 6);
-  }
-  const double* src = partial + ((size_t)qq * G8_N + a) * G8_NS + (b & 63);
-  double s = 0.0;
-  for (int g = 0; g < ngroups; ++g) s += src[(size_t)g * 4 * G8_N * G8_NS];
   gram[e] = s * (c < G8_N ? s_vv : s_vd);
 }
 

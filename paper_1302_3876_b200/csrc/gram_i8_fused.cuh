@@ -7,7 +7,7 @@
 // Groups of 4 CTAs (one per SM, cooperative launch: all co-resident) own a range of
 // 32-row observation blocks.  CTA q of a group:
 //  * slices the blocks t = q (mod 4) of its group into a per-group ring of GFL_RING
-//    images in global memory, small enough to stay in L2 (37 x 16 x 48 KiB = 28 MiB),
+//    images in global memory, small enough to stay in L2 (37 x 32 x 48 KiB = 57 MiB),
 //    written directly in the level-split layout [P_1 Q_1 P_2 Q_2 ... P_6 Q_6];
 //  * consumes EVERY image of the group through one 48 KiB bulk TMA copy per block and
 //    issues the N = 256 kind::i8 MMAs of its level set (G8LS_SETS, as
@@ -18,7 +18,7 @@
 //   slicer  : wait consumed[slot] >= 4 * (t / RING) (previous occupant read by all 4),
 //             write the image; team barrier; leader: fence + release ready[slot] = t + 1
 //   consumer: acquire ready[slot] >= k + 1; fence.proxy.async; bulk copy into a stage;
-//             once it has landed: consumed[slot] += 1 (release)
+//             the MMA issuer, once the copy has landed: consumed[slot] += 1 (release)
 // Every spin is bounded (a deadlock traps instead of hanging the GPU).
 //
 // Slicing (2 teams of 4 warps, thread = member mm of P and Q): per 16-row half-block
@@ -38,11 +38,20 @@
 
 namespace enkf {
 
-constexpr int GFL_RING = 16;      // images per group ring (37 x 16 x 48 KiB = 28 MiB of L2)
-constexpr int GFL_NST = 3;        // MMA smem stages (48 KiB each)
+#ifndef GFL_RING_DEF
+#define GFL_RING_DEF 32
+#endif
+constexpr int GFL_RING = GFL_RING_DEF;  // images per group ring (37 x 32 x 48 KiB = 57 MiB of L2)
+#ifndef GFL_NST_DEF
+#define GFL_NST_DEF 3
+#endif
+#ifndef GFL_TEAMS_DEF
+#define GFL_TEAMS_DEF 2
+#endif
+constexpr int GFL_NST = GFL_NST_DEF;  // MMA smem stages (48 KiB each)
 constexpr int GFL_HB = 16;        // rows per slicer half-block
-constexpr int GFL_TEAMS = 2;      // slicer teams of 4 warps; a team slices whole blocks
-constexpr int GFL_NHB = 4;        // staging depth (half-blocks the loader runs ahead)
+constexpr int GFL_TEAMS = GFL_TEAMS_DEF;  // slicer teams of 4 warps; a team slices whole blocks
+constexpr int GFL_NHB = 2 * GFL_TEAMS;  // staging depth (half-blocks the loader runs ahead)
 constexpr int GFL_XST = GFL_HB * G8_N * 8;       // 16 KiB: X rows of a half-block
 constexpr int GFL_STG = GFL_XST + GFL_HB * 8;    // + r of its rows
 constexpr int GFL_SLW = 4 * GFL_TEAMS;           // slicer warps 0..7
@@ -69,14 +78,38 @@ __device__ __forceinline__ void red_add_release_gpu(int* p, int v) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
-// poll until *p >= target (bounded; trap on a deadlock)
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// poll until *p >= target (bounded; trap on a deadlock).  Relaxed polls (an acquire
+// load invalidates the whole L1 on every try: CCTL.IVALL), then one acquire fence.
 __device__ __forceinline__ void gfl_wait_geq(const int* p, int target) {
   long long spins = 0;
-  while (ld_acquire_gpu(p) < target) {
+  while (ld_relaxed_gpu(p) < target) {
     __nanosleep(32);
     if (++spins > GFL_SPIN_LIMIT) __trap();
   }
+  asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
 }
+
+// profiling only (-DGFL_TRACE_ON): %globaltimer stamps of the roles of group 0
+// (CTAs 0-3) for its first GFL_TRACE_BLOCKS blocks, read by enkf_debug_gfl_trace
+constexpr int GFL_TRACE_BLOCKS = 512;
+__device__ unsigned long long g_gfl_trace[4][GFL_TRACE_BLOCKS][6];
+#ifdef GFL_TRACE_ON
+#define GFL_TRACE(k, ev)                                                                   \
+  do {                                                                                     \
+    if (blockIdx.x < 4 && (k) < GFL_TRACE_BLOCKS) {                                        \
+      unsigned long long _t;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_t));                               \
+      g_gfl_trace[blockIdx.x][(k)][(ev)] = _t;                                             \
+    }                                                                                      \
+  } while (0)
+#else
+#define GFL_TRACE(k, ev) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(GFL_THREADS, 1)
 gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int64_t* __restrict__ idx,
@@ -210,98 +243,122 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     int flags = 0, ovf = 0;
     // 1.5 2^52 + bias: fma(v, sc, kMagicB) holds V + 0x808080808080 in its low 51 bits
     const double kMagicB = 6755399441055744.0 + (double)0x808080808080ull;
-    for (int64_t j = team; j < my_blocks; j += GFL_TEAMS) {
+    auto two_planes = [](const uint32_t (&x)[4], uint32_t bi, uint32_t bj, uint32_t& wi, uint32_t& wj) {
+      const uint32_t sel = bi | ((bi + 4u) << 4) | (bj << 8) | ((bj + 4u) << 12);
+      const uint32_t A = __byte_perm(x[0], x[1], sel);
+      const uint32_t B = __byte_perm(x[2], x[3], sel);
+      wi = __byte_perm(A, B, 0x5410) ^ 0x80808080u;
+      wj = __byte_perm(A, B, 0x7632) ^ 0x80808080u;
+    };
+    // the team's halves in order: i -> block j = team + GFL_TEAMS (i >> 1), half i & 1
+    const int64_t my_team_blocks = my_blocks > team ? (my_blocks - 1 - team) / GFL_TEAMS + 1 : 0;
+    const int64_t nhalf = 2 * my_team_blocks;
+    auto half_row0 = [&](int64_t i) { return (b0 + q + 4 * (team + GFL_TEAMS * (i >> 1))) * G8_KB + GFL_HB * (i & 1); };
+    // Y of a half straight from global memory into registers, one half ahead: the
+    // next half's loads are issued as soon as this half's Q digits are formed, so
+    // their latency overlaps the P digits, the staging wait and the row means
+    double yv[GFL_HB];
+    if (nhalf > 0) {
+      const int64_t g0 = half_row0(0);
+#pragma unroll
+      for (int k = 0; k < GFL_HB; ++k) yv[k] = (g0 + k < n_obs) ? __ldcs(Y + (g0 + k) * G8_N + mm) : 0.0;
+    }
+    for (int64_t i = 0; i < nhalf; ++i) {
+      const int64_t j = team + GFL_TEAMS * (i >> 1);
+      const int h = (int)(i & 1);
       const int64_t t = q + 4 * j;
       const int slot = (int)(t % GFL_RING);
       unsigned char* img = gring + (size_t)slot * G8LS_STAGE;
-      if (t >= GFL_RING) {  // the slot's previous image must be consumed by all 4 CTAs
-        if (mm == 0) gfl_wait_geq(gcons + slot, 4 * (int)(t / GFL_RING));
-        asm volatile("bar.sync %0, 128;\n" ::"r"(2 + team) : "memory");
+      if (h == 0) {
+        if (mm == 0) GFL_TRACE(j, 0);
+        if (t >= GFL_RING) {  // the slot's previous image must be consumed by all 4 CTAs
+          if (mm == 0) gfl_wait_geq(gcons + slot, 4 * (int)(t / GFL_RING));
+          asm volatile("bar.sync %0, 128;\n" ::"r"(2 + team) : "memory");
+        }
+        if (mm == 0) GFL_TRACE(j, 1);
       }
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int64_t hh = 2 * j + h;
-        const int buf = (int)(hh % GFL_NHB);
-        const int64_t g0 = (b0 + t) * G8_KB + GFL_HB * h;
-        // Y of the 16 rows straight from global memory, issued first (latency overlaps
-        // the wait and step A)
-        double yv[GFL_HB];
+      const int64_t hh = 2 * j + h;  // the loader's half index
+      const int buf = (int)(hh % GFL_NHB);
+      mbar_wait(&hfull[buf], (uint32_t)((hh / GFL_NHB) & 1));
+      const double* xs = stg + buf * (GFL_STG / 8);
+      const double* rs = xs + GFL_XST / 8;
+      // step A: row means (warp tw: rows 4tw..4tw+3), sqrt(1/r) (warp 0, lane = row)
 #pragma unroll
-        for (int k = 0; k < GFL_HB; ++k) yv[k] = (g0 + k < n_obs) ? __ldcs(Y + (g0 + k) * G8_N + mm) : 0.0;
-        mbar_wait(&hfull[buf], (uint32_t)((hh / GFL_NHB) & 1));
-        const double* xs = stg + buf * (GFL_STG / 8);
-        const double* rs = xs + GFL_XST / 8;
-        // step A: row means (warp tw: rows 4tw..4tw+3), sqrt(1/r) (warp 0, lane = row)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int row = 4 * tw + u;
-          double sx = (xs[row * G8_N + lane] + xs[row * G8_N + lane + 32]) +
-                      (xs[row * G8_N + lane + 64] + xs[row * G8_N + lane + 96]);
-          sx = warp_sum(sx);
-          if (lane == 0) rmean[buf * GFL_HB + row] = sx * (1.0 / G8_N);
-        }
-        if (tw == 0 && lane < GFL_HB) {
-          double srv = 0.0;  // invalid rows (bad index, past the end) contribute exact zeros
-          if (rvalid[buf * GFL_HB + lane] != 0) {
-            const double rv = rs[lane];
-            if (!isfinite(rv)) flags |= FLAG_NONFINITE;
-            else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
-            srv = g8_sqrt_rho(rv);
-          }
-          rsr[buf * GFL_HB + lane] = srv;
-        }
-        asm volatile("bar.sync %0, 128;\n" ::"r"(2 + team) : "memory");
-        // step B: 16 rows -> the 16-byte chunk h of member mm's row in all 12 planes
-        double xr[GFL_HB];
-#pragma unroll
-        for (int k = 0; k < GFL_HB; ++k) xr[k] = xs[k * G8_N + mm];
-        const size_t off = (size_t)mm * 32 + (size_t)((h ^ ((mm >> 2) & 1)) << 4);
-#pragma unroll
-        for (int pq = 0; pq < 2; ++pq) {
-          uint32_t w[G8_ND][4];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t vlo[4], vhi[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int row = 4 * q4 + u;
-              // the slice pass's exact arithmetic (gram_i8_slice_kernel): the two Gram
-              // forms agree bit for bit
-              const double sr = rsr[buf * GFL_HB + row];
-              const double d = pq == 0 ? xr[row] - rmean[buf * GFL_HB + row] : yv[row] - xr[row];
-              const double tv = fma(sr * d, pq == 0 ? scp : scq, kMagicB);
-              const uint32_t hv = (uint32_t)__double2hiint(tv) - 0x43380000u;
-              ovf |= hv >= 0x10000u;  // V + bias outside [0, 2^48): |V| too large, or non-finite
-              vlo[u] = (uint32_t)__double2loint(tv);
-              vhi[u] = hv;
-            }
-            auto two_planes = [&](const uint32_t (&x)[4], uint32_t bi, uint32_t bj, uint32_t& wi, uint32_t& wj) {
-              const uint32_t sel = bi | ((bi + 4u) << 4) | (bj << 8) | ((bj + 4u) << 12);
-              const uint32_t A = __byte_perm(x[0], x[1], sel);
-              const uint32_t B = __byte_perm(x[2], x[3], sel);
-              wi = __byte_perm(A, B, 0x5410) ^ 0x80808080u;
-              wj = __byte_perm(A, B, 0x7632) ^ 0x80808080u;
-            };
-            two_planes(vhi, 1u, 0u, w[0][q4], w[1][q4]);
-            two_planes(vlo, 3u, 2u, w[2][q4], w[3][q4]);
-            two_planes(vlo, 1u, 0u, w[4][q4], w[5][q4]);
-          }
-          // level-split layout: plane p of P at 2p, of Q at 2p + 1 (x 4 KiB)
-          unsigned char* base = img + (size_t)pq * G8_PLANE + off;
-#pragma unroll
-          for (int p = 0; p < G8_ND; ++p)
-            *reinterpret_cast<uint4*>(base + (size_t)(2 * p) * G8_PLANE) =
-                make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
-        }
-        mbar_arrive(&hempty[buf]);  // staging read: the loader may refill it
+      for (int u = 0; u < 4; ++u) {
+        const int row = 4 * tw + u;
+        double sx = (xs[row * G8_N + lane] + xs[row * G8_N + lane + 32]) +
+                    (xs[row * G8_N + lane + 64] + xs[row * G8_N + lane + 96]);
+        sx = warp_sum(sx);
+        if (lane == 0) rmean[buf * GFL_HB + row] = sx * (1.0 / G8_N);
       }
-      // publish the block: the team's stores precede its barrier; the leader's
-      // gpu-scope fence orders them before the release of ready[slot]
+      if (tw == 0 && lane < GFL_HB) {
+        double srv = 0.0;  // invalid rows (bad index, past the end) contribute exact zeros
+        if (rvalid[buf * GFL_HB + lane] != 0) {
+          const double rv = rs[lane];
+          if (!isfinite(rv)) flags |= FLAG_NONFINITE;
+          else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
+          srv = g8_sqrt_rho(rv);
+        }
+        rsr[buf * GFL_HB + lane] = srv;
+      }
       asm volatile("bar.sync %0, 128;\n" ::"r"(2 + team) : "memory");
-      if (mm == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        st_release_gpu(gready + slot, (int)t + 1);
+      // step B: 16 rows -> the 16-byte chunk h of member mm's row in all 12 planes,
+      // Q first (it frees yv for the next half's loads), then P
+      // (x is re-read from the staging buffer in each pass rather than held in 16
+      // registers: the slicers live at the 128-register cap of this 15-warp CTA)
+      const size_t off = (size_t)mm * 32 + (size_t)((h ^ ((mm >> 2) & 1)) << 4);
+#pragma unroll
+      for (int pq = 1; pq >= 0; --pq) {
+        uint32_t w[G8_ND][4];
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint32_t vlo[4], vhi[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int row = 4 * q4 + u;
+            // the slice pass's exact arithmetic (gram_i8_slice_kernel): the two Gram
+            // forms agree bit for bit
+            const double sr = rsr[buf * GFL_HB + row];
+            const double xv = xs[row * G8_N + mm];
+            const double d = pq == 0 ? xv - rmean[buf * GFL_HB + row] : yv[row] - xv;
+#ifdef GFL_NO_FP64  // timing experiment only (wrong digits): the slicers without FP64 arithmetic
+            const double tv = __hiloint2double(0x43380000 + (__double2hiint(xv) & 0xff),
+                                               __double2loint(xv) ^ __double2loint(yv[row]) ^ row);
+            (void)sr; (void)d;
+#else
+            const double tv = fma(sr * d, pq == 0 ? scp : scq, kMagicB);
+#endif
+            const uint32_t hv = (uint32_t)__double2hiint(tv) - 0x43380000u;
+            ovf |= hv >= 0x10000u;  // V + bias outside [0, 2^48): |V| too large, or non-finite
+            vlo[u] = (uint32_t)__double2loint(tv);
+            vhi[u] = hv;
+          }
+          two_planes(vhi, 1u, 0u, w[0][q4], w[1][q4]);
+          two_planes(vlo, 3u, 2u, w[2][q4], w[3][q4]);
+          two_planes(vlo, 1u, 0u, w[4][q4], w[5][q4]);
+        }
+        // level-split layout: plane p of P at 2p, of Q at 2p + 1 (x 4 KiB)
+        unsigned char* base = img + (size_t)pq * G8_PLANE + off;
+#pragma unroll
+        for (int p = 0; p < G8_ND; ++p)
+          *reinterpret_cast<uint4*>(base + (size_t)(2 * p) * G8_PLANE) = make_uint4(w[p][0], w[p][1], w[p][2], w[p][3]);
+        if (pq == 1 && i + 1 < nhalf) {  // prefetch the next half's Y
+          const int64_t g1 = half_row0(i + 1);
+#pragma unroll
+          for (int k = 0; k < GFL_HB; ++k) yv[k] = (g1 + k < n_obs) ? __ldcs(Y + (g1 + k) * G8_N + mm) : 0.0;
+        }
+      }
+      mbar_arrive(&hempty[buf]);  // staging read: the loader may refill it
+      if (h == 1) {
+        // publish the block: the team's stores precede its barrier; the leader's
+        // gpu-scope fence orders them before the release of ready[slot]
+        asm volatile("bar.sync %0, 128;\n" ::"r"(2 + team) : "memory");
+        if (mm == 0) {
+          __threadfence();
+          fence_proxy_async_global();
+          st_release_gpu(gready + slot, (int)t + 1);
+          GFL_TRACE(j, 2);
+        }
       }
     }
     flags = __reduce_or_sync(0xffffffffu, flags);
@@ -312,25 +369,38 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
     }
   } else if (warp == GFL_MPW) {
     // ---- MMA producer: ring image -> smem stage (one 48 KiB bulk copy) ---------------
-    if (lane == 0) {
-      for (int64_t k = 0; k < nblk; ++k) {
-        const int st = (int)(k % GFL_NST);
-        const int slot = (int)(k % GFL_RING);
-        if (k >= GFL_NST) mbar_wait(&sempty[st], (uint32_t)(((k / GFL_NST) - 1) & 1));
-        gfl_wait_geq(gready + slot, (int)k + 1);
+    // (the MMA issuer releases each ring slot once its copy has landed, so the
+    // producer never waits on a copy: up to GFL_NST copies in flight).  Readiness is
+    // checked for up to 32 blocks at once (lane i: block k + i) with relaxed loads
+    // and one acquire fence per batch: a per-block acquire poll costs an L2 round
+    // trip plus a fence (~1 us) on the producer's critical path.
+    int64_t avail = -1;  // every block <= avail is known to be published
+    long long spins = 0;
+    for (int64_t k = 0; k < nblk; ++k) {
+      const int st = (int)(k % GFL_NST);
+      const int slot = (int)(k % GFL_RING);
+      if (k >= GFL_NST) mbar_wait(&sempty[st], (uint32_t)(((k / GFL_NST) - 1) & 1));
+      GFL_TRACE(k, 3);
+      while (k > avail) {
+        const int64_t kk = k + lane;
+        const bool ok = kk >= nblk || (lane < GFL_RING && ld_relaxed_gpu(gready + (int)(kk % GFL_RING)) >= (int)kk + 1);
+        const unsigned ball = __ballot_sync(0xffffffffu, ok);
+        const int run = ball == 0xffffffffu ? 32 : __ffs(~ball) - 1;  // leading published blocks
+        if (run > 0) {
+          avail = k + run - 1;
+          asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+        } else {
+          __nanosleep(32);
+          if (++spins > GFL_SPIN_LIMIT) __trap();
+        }
+      }
+      GFL_TRACE(k, 4);
+      if (lane == 0) {
         fence_proxy_async_global();
         mbar_arrive_expect_tx(&sfull[st], (uint32_t)G8LS_STAGE);
         bulk_g2s(stages + st * G8LS_STAGE, gring + (size_t)slot * G8LS_STAGE, (uint32_t)G8LS_STAGE, &sfull[st]);
-        // the previous image is in shared memory: its ring slot may be refilled
-        if (k >= 1) {
-          mbar_wait(&sfull[(k - 1) % GFL_NST], (uint32_t)(((k - 1) / GFL_NST) & 1));
-          red_add_release_gpu(gcons + (int)((k - 1) % GFL_RING), 1);
-        }
       }
-      if (nblk >= 1) {
-        mbar_wait(&sfull[(nblk - 1) % GFL_NST], (uint32_t)(((nblk - 1) / GFL_NST) & 1));
-        red_add_release_gpu(gcons + (int)((nblk - 1) % GFL_RING), 1);
-      }
+      __syncwarp();
     }
   } else if (warp == GFL_MMAW) {
     // ---- MMA issuer: one N = 256 MMA per digit pair of the CTA's level set
@@ -341,6 +411,9 @@ gram_i8_fused_kernel(const double* __restrict__ X, const double* __restrict__ Y,
       const bool first_in_period = (k % G8_FLUSH_BLOCKS) == 0;
       if (first_in_period && k > 0) mbar_wait(aempty, (uint32_t)(((k / G8_FLUSH_BLOCKS) - 1) & 1));
       mbar_wait(&sfull[slot], (uint32_t)((k / GFL_NST) & 1));
+      if (lane == 0) GFL_TRACE(k, 5);
+      // the image is in shared memory: its ring slot may be refilled
+      if (lane == 0) red_add_release_gpu(gcons + (int)(k % GFL_RING), 1);
       tc_fence_after();
       const uint32_t st = sbase + (uint32_t)(slot * G8LS_STAGE);
       bool fresh0 = first_in_period, fresh1 = first_in_period;
