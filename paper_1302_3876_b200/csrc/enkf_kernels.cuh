@@ -1150,15 +1150,19 @@ __device__ long long g_lv_trace[20][6];
 #define LV_TRACE(blk, ph) do { } while (0)
 #endif
 #ifndef LV_SERIAL_LDL
-#define LV_SERIAL_LDL 1  // pivot-block LDL' by one thread in registers (0: the warp-shuffle form)
+#define LV_SERIAL_LDL 1  // pivot-block LDL' by one thread in registers (0: the warp-shuffle form; an
+                         // in-place shared-memory form was measured 1.4x slower over the kernel)
 #endif
 #ifndef LV_THREADS
 #define LV_THREADS 512  // 128 registers per thread: the 1024-thread form spilled (ncu: STL in the trailing update)
 #endif
 
 __host__ __device__ inline int64_t levels_blk_smem_doubles(int n) {
-  return levels_vv_doubles(n) + (int64_t)n * n /*VD*/ + (int64_t)LB * n /*PT*/ +
-         (int64_t)LB * 2 * n /*R/Q*/ + (int64_t)LB * LB /*L*/ + 2 * LB /*D, 1/D*/ + n /*colmean*/ + 16;
+  // (V'D lives in registers and leaves through them: no [n][n] buffer, so the kernel
+  // leaves ~140 KiB of the SM's 256 KiB to L1, where the fragments that do not fit
+  // in registers live)
+  return levels_vv_doubles(n) + (int64_t)LB * n /*PT*/ + (int64_t)LB * 2 * n /*R/Q*/ + (int64_t)LB * LB /*L*/ +
+         2 * LB /*D, 1/D*/ + 4 * (int64_t)n /*column partials*/ + n /*colmean*/ + 16;
 }
 
 __global__ void __launch_bounds__(LV_THREADS, 1)
@@ -1169,12 +1173,12 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
   double* vv = bsm;                                  // packed upper V'V: p(i,c) = c(c+1)/2 + i
-  double* vd = vv + levels_vv_doubles(n);            // [n][n]    V'D (A after the last level)
-  double* PT = vd + (int64_t)n * n;                  // [LB][n]   Gamma[i][k0+j] at PT[j][i]
+  double* PT = vv + levels_vv_doubles(n);            // [LB][n]   Gamma[i][k0+j] at PT[j][i]
   double* RQ = PT + LB * n;                          // [LB][2n]  R, then Q = M^-1 R
   double* Lm = RQ + LB * 2 * n;                      // [LB][LB]  unit lower factor
   double* Dm = Lm + LB * LB;                         // [LB]      pivots
-  double* cm = Dm + 2 * LB;                          // [n]       column means (epilogue)
+  double* cpart = Dm + 2 * LB;                       // [4][n]    column partial sums (epilogue)
+  double* cm = cpart + 4 * n;                        // [n]       column means (epilogue)
   int* fail = reinterpret_cast<int*>(cm + n);
   auto P = [](int i, int c) { return c * (c + 1) / 2 + i; };
   const int n2 = 2 * n;
@@ -1384,29 +1388,41 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
   }
 
   LV_TRACE(16, 0);
+  // A = V'Z straight from the fragments; T = I + cscale (A - 1 colmean(A)'), the column
+  // sums in a fixed order: per warp over its 32 rows (fragment rows, then shuffles
+  // over the 8 row lanes), then the 4 row blocks in order
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int e = 0; e < 2; ++e) {
+      const int c = 32 * wn + 8 * nt + 2 * fk + e;
+      double cs = 0.0;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int i = 32 * wm + 8 * mt + fr, c = 32 * wn + 8 * nt + 2 * fk + e;
-        if (i < n && c < n) vd[i * n + c] = vdr[mt][nt][e];
+      for (int mt = 0; mt < 4; ++mt) {
+        const int i = 32 * wm + 8 * mt + fr;
+        if (i < n && c < n) {
+          A[i * n + c] = vdr[mt][nt][e];
+          cs += vdr[mt][nt][e];
+        }
       }
-  __syncthreads();
-  // A = V'Z; T = I + cscale (A - 1 colmean(A)')
-  for (int e = tid; e < n * n; e += nthr) A[e] = vd[e];
+      cs += __shfl_xor_sync(0xffffffffu, cs, 4);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 8);
+      cs += __shfl_xor_sync(0xffffffffu, cs, 16);
+      if (fr == 0 && c < n) cpart[wm * n + c] = cs;
+    }
   if (T != nullptr) {
-    for (int c = tid; c < n; c += nthr) {
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s += vd[i * n + c];
-      cm[c] = s / (double)n;
-    }
     __syncthreads();
-    for (int e = tid; e < n * n; e += nthr) {
-      const int i = e / n, c = e - i * n;
-      T[e] = (i == c ? 1.0 : 0.0) + cscale * (vd[e] - cm[c]);
-    }
+    for (int c = tid; c < n; c += nthr) cm[c] = (((cpart[c] + cpart[n + c]) + cpart[2 * n + c]) + cpart[3 * n + c]) / (double)n;
+    __syncthreads();
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = 32 * wm + 8 * mt + fr, c = 32 * wn + 8 * nt + 2 * fk + e;
+          if (i < n && c < n) T[i * n + c] = (i == c ? 1.0 : 0.0) + cscale * (vdr[mt][nt][e] - cm[c]);
+        }
   }
 }
 
