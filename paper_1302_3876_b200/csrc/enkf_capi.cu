@@ -23,6 +23,7 @@
 #include "host_stream.cuh"
 #include "tiny.cuh"
 #include "nccl_comm.cuh"
+#include "levels_cluster.cuh"
 
 using namespace enkf;
 
@@ -38,6 +39,7 @@ struct enkf_plan {
   bool anomaly_i8 = true;      // tensor-core (int8 digit) anomaly update, N == 128
   int i8_dbg = 0;              // profiling-only role skips (ENKF_I8_DBG)
   bool levels_blocked = true;  // blocked (LB levels per barrier) Sherman-Morrison recursion
+  bool levels_cluster = true;  // ... on a 4-CTA cluster (ENKF_LEVELS=single: one CTA; =level: level by level)
   bool host_streamed = true;   // pipelined host path for pinned X / XA (ENKF_HOST_STREAM=0 disables)
   size_t host_chunk_bytes = (size_t)256 << 20;
   bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
@@ -366,6 +368,26 @@ cudaError_t launch_tiny(const enkf_plan* p, const double* X, const double* Y, co
 
 cudaError_t launch_levels(const enkf_plan* p, const double* gram, double* A, double* T,
                           double* den, double cscale, cudaStream_t s) {
+  if (p->levels_cluster && p->n >= 2 && p->n <= 128) {
+    // the blocked recursion on a cluster of LC_CTAS CTAs (levels_cluster.cuh)
+    const size_t smem = (size_t)levels_cluster_smem_doubles(p->n) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(ism_levels_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(LC_CTAS);
+    cfg.blockDim = dim3(LC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = LC_CTAS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, ism_levels_cluster_kernel, gram, p->n, cscale, A, T, den, p->dstatus);
+  }
   if (p->levels_blocked) {
     const size_t smem = (size_t)levels_blk_smem_doubles(p->n) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(ism_levels_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -711,7 +733,10 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
 #ifdef I8_DBG_BUILD  // profiling variants only (tools/build_variant.py NAME -DI8_DBG_BUILD)
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
 #endif
-  if (const char* env = getenv("ENKF_LEVELS")) p->levels_blocked = (strcmp(env, "level") != 0);
+  if (const char* env = getenv("ENKF_LEVELS")) {
+    p->levels_blocked = (strcmp(env, "level") != 0);
+    p->levels_cluster = (strcmp(env, "level") != 0 && strcmp(env, "single") != 0);
+  }
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
     p->gram_fused = (strcmp(env, "i8fused") == 0);

@@ -1201,6 +1201,7 @@ ism_levels_blocked_kernel(const double* __restrict__ gram, int n, double cscale,
         const int i = 32 * wm + 8 * mt + fr, c = 32 * wn + 8 * nt + 2 * fk + e;
         vdr[mt][nt][e] = (i < n && c < n) ? gram[(int64_t)i * n2 + n + c] : 0.0;
       }
+  for (int e = tid; e < LB * LB; e += nthr) Lm[e] = 0.0;  // rows of a short last block stay finite
   if (tid == 0) *fail = 0;
   __syncthreads();
 

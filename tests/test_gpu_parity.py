@@ -540,6 +540,66 @@ def test_fused_gram_equals_two_kernel_gram(sizes):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("n", [2, 5, 8, 20, 31, 64, 96, 97, 127, 128])
+def test_levels_cluster_equals_single_cta(n, monkeypatch):
+    """The N Sherman-Morrison levels on a 4-CTA cluster (default; V'V columns and V'D
+    bands split over the CTAs, pivot columns exchanged through distributed shared
+    memory) perform the single-CTA kernel's arithmetic in the same order: A, T and
+    every den_k agree bit for bit, and A matches a dense solve of (I + V'V) A = V'D."""
+    import torch
+    dev = torch.device("cuda", 0)
+    g = np.random.Generator(np.random.Philox(40 + n))
+    v = g.standard_normal((3000, n)) / np.sqrt(max(n - 1, 1))
+    d = g.standard_normal((3000, n))
+    gram = np.concatenate([v.T @ v, v.T @ d / np.sqrt(max(n - 1, 1))], axis=1)
+    gd = torch.from_numpy(gram).to(dev)
+    s = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for mode in ("single", "cluster"):
+        monkeypatch.setenv("ENKF_LEVELS", mode)
+        plan = _native.Plan(1, 1, n, 0)
+        a = torch.full((n, n), float("nan"), dtype=torch.float64, device=dev)
+        t = torch.full_like(a, float("nan"))
+        den = torch.full((n,), float("nan"), dtype=torch.float64, device=dev)
+        assert _native.lib().enkf_plan_reset_status(plan.handle, s) == 0
+        assert _native.lib().enkf_ism_levels_f64(plan.handle, gd.data_ptr(), a.data_ptr(), t.data_ptr(),
+                                                 den.data_ptr(), s) == 0
+        st = _native.EnkfStatus()
+        assert _native.lib().enkf_plan_sync_status(plan.handle, s, ctypes.byref(st)) == 0, st.message
+        out[mode] = (a.cpu().numpy(), t.cpu().numpy(), den.cpu().numpy())
+    monkeypatch.delenv("ENKF_LEVELS")
+    for k in range(3):
+        assert np.array_equal(out["single"][k], out["cluster"][k]), (n, k)
+    ref = np.linalg.solve(np.eye(n) + gram[:, :n], gram[:, n:])
+    assert np.abs(out["cluster"][0] - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_levels_cluster_singular_level(monkeypatch):
+    """The singular guard (sherman.py:171-174) on the cluster kernel: the first failing
+    1-based level and its denominator, as the single-CTA kernel reports them."""
+    import torch
+    dev = torch.device("cuda", 0)
+    n = 40
+    gram = np.zeros((n, 2 * n))
+    gram[:, :n] = np.eye(n)
+    gram[17, 17] = -1.0  # den_18 = 1 + (-1) = 0
+    gd = torch.from_numpy(gram).to(dev)
+    s = torch.cuda.current_stream().cuda_stream
+    res = {}
+    for mode in ("single", "cluster"):
+        monkeypatch.setenv("ENKF_LEVELS", mode)
+        plan = _native.Plan(1, 1, n, 0)
+        a = torch.empty((n, n), dtype=torch.float64, device=dev)
+        _native.lib().enkf_plan_reset_status(plan.handle, s)
+        _native.lib().enkf_ism_levels_f64(plan.handle, gd.data_ptr(), a.data_ptr(), None, None, s)
+        st = _native.EnkfStatus()
+        code = _native.lib().enkf_plan_sync_status(plan.handle, s, ctypes.byref(st))
+        res[mode] = (code, st.level, st.denominator)
+    monkeypatch.delenv("ENKF_LEVELS")
+    assert res["cluster"] == res["single"] and res["cluster"][0] == _native.ENKF_SINGULAR_UPDATE
+    assert res["cluster"][1] == 18
+
+
 def test_anomaly_debug_env_has_no_effect(monkeypatch):
     """The profiling role skips of anomaly_i8_kernel are compiled out of the product
     library: ENKF_I8_DBG set at plan creation changes nothing (bitwise)."""
