@@ -115,6 +115,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
     const int c0 = k0 + b;
     const double* PT = PTb + (blk & 1) * LB * n;
     double* PTn = PTb + ((blk + 1) & 1) * LB * n;
+    if (r == 0) LV_TRACE(blk, 0);
     // ---- 1. R for the own trailing V'V columns and the own V'D columns
     for (int e = tid; e < b * mown; e += LC_THREADS) {
       const int j = e / mown, m = e - j * mown, c = LC_CTAS * m + r;
@@ -134,6 +135,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
       }
     }
     // ---- 2. LDL' of M = I + Gamma[K, K] (every CTA the same), one thread in registers
+    if (r == 0) LV_TRACE(blk, 1);
     if (tid == 0) {
       double m[LB][LB];
 #pragma unroll
@@ -168,6 +170,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
       }
     }
     __syncthreads();
+    if (r == 0) LV_TRACE(blk, 2);
     if (*fail) return;  // uniform across the cluster: every CTA factors the same block
     // ---- 3. Q = M^-1 R, one own column per thread (V'V trailing, then V'D)
     for (int t = tid; t < mown + w; t += LC_THREADS) {
@@ -200,6 +203,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
         if (j < b) col[j * ld] = y[j];
     }
     __syncthreads();
+    if (r == 0) LV_TRACE(blk, 3);
     // ---- 4. rank-b update of the own trailing V'V columns (warp per column) and V'D
 #pragma unroll 1
     for (int m = warp; m < mown; m += LC_THREADS / 32) {
@@ -239,6 +243,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
     }
     if (c0 >= n) break;
     __syncthreads();  // own columns updated
+    if (r == 0) LV_TRACE(blk, 4);
     // ---- 5. push the next block's pivot columns Gamma[:, c0..c0+b'-1] to every CTA:
     //      the owner of column c writes Gamma[c0+j][c] (c >= c0 + j) and, for a pivot
     //      column c = c0 + j, its rows 0..c-1 as well
@@ -268,6 +273,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
         lc_st_remote(lc_mapa(PTn + j * n + i, (uint32_t)dst), v);
       }
     }
+    if (r == 0) LV_TRACE(blk, 5);
     lc_cluster_sync();
   }
 
