@@ -1,7 +1,7 @@
 """A/B of the Gram forms at config 5 (or 2^-s of it): the Gram alone and the whole
 step, per ENKF_GRAM mode, alternating, CUDA events; Grams compared bitwise.
 
-    python tools/probe/gram_ab.py [scale_log2] [modes, e.g. i8ls,i8fused] [reps]
+    python tools/probe/gram_ab.py [scale_log2] [modes, e.g. i8ls,i8fused,i8ls:1024] [reps]
 """
 import ctypes
 import json
@@ -26,9 +26,12 @@ x, y, idx, r = d["x"], d["perturbed"], d["idx"], d["r"]
 ns, no, n = x.shape[0], y.shape[0], x.shape[1]
 xa = torch.empty_like(x)
 plans = {}
-for m in modes:
-    os.environ["ENKF_GRAM"] = m
+for m in modes:  # "mode" or "mode:chunk_blocks" (ENKF_GRAM_CHUNK)
+    os.environ["ENKF_GRAM"] = m.split(":")[0]
+    if ":" in m:
+        os.environ["ENKF_GRAM_CHUNK"] = m.split(":")[1]
     plans[m] = _native.Plan(ns, no, n, 0)
+    os.environ.pop("ENKF_GRAM_CHUNK", None)
 os.environ.pop("ENKF_GRAM", None)
 gram = {m: torch.empty((n, 2 * n), dtype=torch.float64, device=dev) for m in modes}
 res = {m: {"gram_ms": [], "step_ms": []} for m in modes}
