@@ -110,30 +110,37 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
   __syncthreads();
   lc_cluster_sync();  // every CTA's buffers initialised before any remote store
 
+  // R = Gamma[K, own trailing columns] for the block K = [kk0, kk0 + bb): rows of the own
+  // V'V columns and of the own V'D fragments
+  auto gather = [&](int kk0, int bb, int cc0) {
+    for (int e = tid; e < bb * mown; e += LC_THREADS) {
+      const int j = e / mown, m = e - j * mown, c = LC_CTAS * m + r;
+      if (c >= cc0) Rv[j * rv_ld + m] = vv[lc_off(m, r) + kk0 + j];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int i = 32 * wm + 8 * mt + fr;
+      if (i >= kk0 && i < kk0 + bb) {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl = (w / 2) * wn + 8 * nt + 2 * fk + e;
+            if (nt < ntn) Rd[(i - kk0) * 32 + cl] = vdr[mt][nt][e];
+          }
+      }
+    }
+  };
+  gather(0, n < LB ? n : LB, n < LB ? n : LB);
+  __syncthreads();
+
   for (int k0 = 0, blk = 0; k0 < n; k0 += LB, ++blk) {
     const int b = (n - k0) < LB ? (n - k0) : LB;
     const int c0 = k0 + b;
     const double* PT = PTb + (blk & 1) * LB * n;
     double* PTn = PTb + ((blk + 1) & 1) * LB * n;
     if (r == 0) LV_TRACE(blk, 0);
-    // ---- 1. R for the own trailing V'V columns and the own V'D columns
-    for (int e = tid; e < b * mown; e += LC_THREADS) {
-      const int j = e / mown, m = e - j * mown, c = LC_CTAS * m + r;
-      if (c >= c0) Rv[j * rv_ld + m] = vv[lc_off(m, r) + k0 + j];
-    }
-#pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
-      const int i = 32 * wm + 8 * mt + fr;
-      if (i >= k0 && i < k0 + b) {
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int cl = (w / 2) * wn + 8 * nt + 2 * fk + e;
-            if (nt < ntn) Rd[(i - k0) * 32 + cl] = vdr[mt][nt][e];
-          }
-      }
-    }
+    // (1. R for this block was gathered at the end of the previous one)
     // ---- 2. LDL' of M = I + Gamma[K, K] (every CTA the same), one thread in registers
     if (r == 0) LV_TRACE(blk, 1);
     if (tid == 0) {
@@ -221,6 +228,43 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
         col[i] = acc;
       }
     }
+    if (c0 < n) {
+      __syncthreads();  // own V'V columns updated
+      if (r == 0) LV_TRACE(blk, 4);
+      // ---- 5. push the next block's pivot columns Gamma[:, c0..c0+b'-1] to every CTA:
+      //      the owner of column c writes Gamma[c0+j][c] (c >= c0 + j) and, for a pivot
+      //      column c = c0 + j, its rows 0..c-1 as well
+      const int bn = (n - c0) < LB ? (n - c0) : LB;
+      for (int m = warp; m < mown; m += LC_THREADS / 32) {
+        const int c = LC_CTAS * m + r;
+        if (c < c0) continue;
+        const double* col = vv + lc_off(m, r);
+        const bool pivot = c < c0 + bn;
+        const int nrow = pivot ? c + 1 : 0;  // full column for a pivot column
+        // items: (j, row c0 + j) for j < bn with c0 + j <= c, then the pivot column rows
+        const int nj = (c - c0 + 1) < bn ? (c - c0 + 1) : bn;
+        for (int it = lane; it < LC_CTAS * (nj + nrow); it += 32) {
+          const int dst = it % LC_CTAS, e = it / LC_CTAS;
+          int j, i;
+          double v;
+          if (e < nj) {
+            j = e;
+            i = c;
+            v = col[c0 + e];
+          } else {
+            j = c - c0;
+            i = e - nj;
+            if (i == c) continue;  // the diagonal entry is item j = c - c0 above
+            v = col[i];
+          }
+          lc_st_remote(lc_mapa(PTn + j * n + i, (uint32_t)dst), v);
+        }
+      }
+      if (r == 0) LV_TRACE(blk, 5);
+      // the cluster barrier in two halves: arrive (release: the pushes) now, wait after
+      // the V'D update and the next block's gather, which overlap its latency
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    }
 #pragma unroll
     for (int ks = 0; ks < LB / 4; ++ks) {
       const int j = 4 * ks + fk;
@@ -242,39 +286,13 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
           if (nt < ntn) dmma884(vdr[mt][nt][0], vdr[mt][nt][1], a[mt], bq[nt]);
     }
     if (c0 >= n) break;
-    __syncthreads();  // own columns updated
-    if (r == 0) LV_TRACE(blk, 4);
-    // ---- 5. push the next block's pivot columns Gamma[:, c0..c0+b'-1] to every CTA:
-    //      the owner of column c writes Gamma[c0+j][c] (c >= c0 + j) and, for a pivot
-    //      column c = c0 + j, its rows 0..c-1 as well
-    const int bn = (n - c0) < LB ? (n - c0) : LB;
-    for (int m = warp; m < mown; m += LC_THREADS / 32) {
-      const int c = LC_CTAS * m + r;
-      if (c < c0) continue;
-      const double* col = vv + lc_off(m, r);
-      const bool pivot = c < c0 + bn;
-      const int nrow = pivot ? c + 1 : 0;  // full column for a pivot column
-      // items: (j, row c0 + j) for j < bn with c0 + j <= c, then the pivot column rows
-      const int nj = (c - c0 + 1) < bn ? (c - c0 + 1) : bn;
-      for (int it = lane; it < LC_CTAS * (nj + nrow); it += 32) {
-        const int dst = it % LC_CTAS, e = it / LC_CTAS;
-        int j, i;
-        double v;
-        if (e < nj) {
-          j = e;
-          i = c;
-          v = col[c0 + e];
-        } else {
-          j = c - c0;
-          i = e - nj;
-          if (i == c) continue;  // the diagonal entry is item j = c - c0 above
-          v = col[i];
-        }
-        lc_st_remote(lc_mapa(PTn + j * n + i, (uint32_t)dst), v);
-      }
+    __syncthreads();  // Q (Rd) read by every warp's DMMA before the next gather overwrites it
+    {
+      const int bn = (n - c0) < LB ? (n - c0) : LB;
+      gather(c0, bn, c0 + bn);
     }
-    if (r == 0) LV_TRACE(blk, 5);
-    lc_cluster_sync();
+    __syncthreads();
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
 
   // ---- A = V'Z from the fragments; T = I + cscale (A - 1 colmean(A)') for the own columns
