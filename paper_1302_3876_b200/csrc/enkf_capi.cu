@@ -386,7 +386,11 @@ cudaError_t launch_levels(const enkf_plan* p, const double* gram, double* A, dou
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, ism_levels_cluster_kernel, gram, p->n, cscale, A, T, den, p->dstatus);
+    e = cudaLaunchKernelEx(&cfg, ism_levels_cluster_kernel, gram, p->n, cscale, A, T, den, p->dstatus);
+    if (e == cudaSuccess) return e;
+    // a context that cannot place a 4-CTA cluster (SM-limited partitions, MPS):
+    // the one-CTA kernel computes the same bits
+    cudaGetLastError();
   }
   if (p->levels_blocked) {
     const size_t smem = (size_t)levels_blk_smem_doubles(p->n) * sizeof(double);
