@@ -782,6 +782,11 @@ def run_reference(args):
         "impl": "reference",
         "cpu_baseline": cpu,
         "e2e": {"value": cpu["value"], "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # configs 4/5 do not fit a host-run of the full workload (config 5 needs ~300 GB and
+        # minutes per step): each timed step is a row sample, the value the full-size
+        # throughput extrapolated linearly (the `linearity` object shows two sample sizes)
+        "extrapolated": bool(cpu.get("extrapolated")),
+        "measured_seconds_per_sample_step": cpu.get("sample_seconds"),
     }
     print(json.dumps(line), flush=True)
 
