@@ -670,10 +670,18 @@ def run_ours(args):
 
     # the whole step on its compulsory bytes (SURVEY §8(d) B_step)
     b_step = 8.0 * (2 * ns * n + 2 * nobs * n + 2 * nobs)
+    f_step = 6.0 * (n * n * nobs + n * nobs) + 2.0 * n * n * nobs + 2.0 * n * n * ns
+    t_floor = max(b_step / (peak * shard_world * 1e9), f_step / (FP64_DMMA_PEAK_TFLOPS * shard_world * 1e12))
     roofline_step = {"bound": "hbm", "unit": "GB/s", "bytes": b_step,
                      "achieved": b_step / (ms_step * 1e-3) / 1e9, "peak": peak * shard_world,
                      "frac": b_step / (ms_step * 1e-3) / 1e9 / (peak * shard_world),
-                     "algorithmic": "B_step = 8*(2*Ns*N + 2*Nobs*N + 2*Nobs): read X, write X^A, read X[idx] rows, Y, r, idx"}
+                     "algorithmic": "B_step = 8*(2*Ns*N + 2*Nobs*N + 2*Nobs): read X, write X^A, read X[idx] rows, Y, r, idx",
+                     # achieved = max(B_step / P_hbm, F_step / P_fp64) / t_step, with
+                     # F_step = 6(N^2 Nobs + N Nobs) + 2 N^2 Nobs + 2 N^2 Ns; > 1 means faster than an
+                     # FP64 implementation could be (the int8-digit emulation)
+                     "survey_formula": {"f_step_flop": f_step, "floor_ms": t_floor * 1e3,
+                                        "achieved": t_floor / (ms_step * 1e-3),
+                                        "p_fp64_tflops": FP64_DMMA_PEAK_TFLOPS}}
 
     ism = None
     comp_row = 2 * n * 8 + 16
