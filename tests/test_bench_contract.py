@@ -65,3 +65,31 @@ def test_gpus_beyond_visible_fails():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--steps", "1"],
                          capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode != 0 and "64" in out.stderr
+
+
+def test_reference_arm_small_config_not_extrapolated():
+    """Configs 1-3 run the oracle on the full configuration: no extrapolation."""
+    d = _run(["--impl", "reference", "--config", "1", "--steps", "2", "--warmup", "0"])
+    assert d["impl"] == "reference" and d["extrapolated"] is False
+    assert d["config"]["workload"].startswith("config1") and d["value"] > 0
+
+
+def test_reference_arm_flags_extrapolation():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0", "--scale-log2", "8"])
+    assert d["extrapolated"] is True and d["measured_seconds_per_sample_step"] > 0
+    lin = d["cpu_baseline"]["linearity"]
+    assert len(lin["seconds"]) == 2 and all(t > 0 for t in lin["seconds"])
+
+
+def test_nccl_init_lines_parsing(tmp_path):
+    """rank 0 folds the per-rank NCCL communicator-init lines into its JSON line."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    (tmp_path / "nccl.host.1.log").write_text("host:1:1 NCCL INFO Bootstrap\n"
+                                              "host:1:1 NCCL INFO ncclCommInitRank comm 0x1 rank 0 nranks 2 - Init COMPLETE\n")
+    (tmp_path / "nccl.host.2.log").write_text("host:2:2 NCCL INFO ncclCommInitRank comm 0x2 rank 1 nranks 2 - Init COMPLETE\n")
+    lines = bench.nccl_init_lines(str(tmp_path))
+    assert len(lines) == 2 and all("nranks 2" in ln for ln in lines)
+    assert bench.nccl_init_lines(None) is None
