@@ -3,6 +3,7 @@
 #include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
+#include <chrono>
 #include <type_traits>
 #include <cmath>
 #include <cstdio>
@@ -81,12 +82,16 @@ struct enkf_plan {
   cudaStream_t hs_in = nullptr, hs_out = nullptr;
   cudaEvent_t ev_obs = nullptr, ev_anom = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
-  // pinned staging ring for pageable host buffers
+  // pinned staging rings for pageable host buffers (ring: inbound / any; oring: X^A outbound)
+  char* oring[2] = {nullptr, nullptr};
+  cudaEvent_t oring_ev[2] = {nullptr, nullptr};
+  size_t pageable_stream_min = (size_t)1 << 30;  // X bytes from which pageable calls stream (ENKF_HOST_STREAM_MIN_MB)
   char* ring[2] = {nullptr, nullptr};
   cudaEvent_t ring_ev[2] = {nullptr, nullptr};
   bool ring_busy[2] = {false, false};  // an async DMA may still touch the slot
   int ring_next = 0;
   size_t ring_bytes = 0;
+  size_t ring_bytes_cfg = (size_t)256 << 20;  // slot size (ENKF_HOST_RING_MB; small values for tests)
   // localized-analysis workspace (lazily allocated): V, D, Z [n_obs][n]
   double* locV = nullptr;
   double* locD = nullptr;
@@ -510,7 +515,7 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 
 cudaError_t ensure_ring(enkf_plan* p) {
   if (p->ring[0]) return cudaSuccess;
-  p->ring_bytes = (size_t)256 << 20;
+  p->ring_bytes = p->ring_bytes_cfg;
   for (int i = 0; i < 2; ++i) {
     cudaError_t e = cudaMallocHost(&p->ring[i], p->ring_bytes);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->ring_ev[i], cudaEventDisableTiming);
@@ -583,6 +588,30 @@ cudaError_t copy_d2h(enkf_plan* p, void* dst, const void* src, size_t bytes, cud
     if (k + 2 < nchunks && (e = launch(k + 2)) != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// Rows idx[0..nrows) of the row-major [*][row_bytes] host array src, gathered into
+// dst by a pool of threads (the observed rows of a pageable X).
+void parallel_gather_rows(char* dst, const char* src, const int64_t* idx, int64_t nrows, size_t row_bytes) {
+  unsigned nt = std::thread::hardware_concurrency();
+  if (nt == 0) nt = 1;
+  if (nt > 16) nt = 16;
+  if ((int64_t)nt > nrows / 1024) nt = (unsigned)(nrows / 1024 > 0 ? nrows / 1024 : 1);
+  auto run = [=](int64_t lo, int64_t hi) {
+    for (int64_t k = lo; k < hi; ++k) memcpy(dst + (size_t)k * row_bytes, src + (size_t)idx[k] * row_bytes, row_bytes);
+  };
+  if (nt <= 1) {
+    run(0, nrows);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int64_t per = (nrows + nt - 1) / nt;
+  for (unsigned t = 0; t < nt; ++t) {
+    const int64_t lo = t * per, hi = lo + per < nrows ? lo + per : nrows;
+    if (lo >= hi) break;
+    th.emplace_back(run, lo, hi);
+  }
+  for (auto& t : th) t.join();
 }
 
 int translate_status(const enkf_plan* p, enkf_status* st) {
@@ -750,6 +779,11 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   if (const char* env = getenv("ENKF_TINY")) p->tiny = (env[0] != '0');
   if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
   if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
+  if (const char* env = getenv("ENKF_HOST_STREAM_MIN_MB")) p->pageable_stream_min = (size_t)atol(env) << 20;
+  if (const char* env = getenv("ENKF_HOST_RING_MB")) {
+    const size_t mb = (size_t)atol(env);
+    p->ring_bytes_cfg = (mb > 0 ? mb : 1) << 20;
+  }
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
 
   // gram128 split: the V'V CTAs do 3/4 of the DMMA work of the V'D CTAs (and
@@ -845,6 +879,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
     if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
+    if (p->oring[i]) cudaFreeHost(p->oring[i]);
+    if (p->oring_ev[i]) cudaEventDestroy(p->oring_ev[i]);
   }
   delete p;
 }
@@ -1075,6 +1111,148 @@ int analysis_host_streamed(enkf_plan* p, const double* X_h, const double* Xmap, 
   }
   return ENKF_OK;
 }
+// Host-buffer analysis with the caller's ordinary (pageable) X and X^A: the same
+// schedule as analysis_host_streamed through pinned staging rings.  The observed rows
+// X[idx] are gathered on the host (thread pool) into the inbound ring and copied in
+// first; the Gram and the levels run on them; then X streams in chunk by chunk (host
+// copy into an inbound ring slot, DMA), each chunk's anomaly update runs as it lands,
+// and its X^A returns through the outbound ring while the next chunk comes in — the
+// two PCIe directions and the host copies overlap.  Bound by host-memory copy
+// bandwidth (both directions pass through the rings).
+int analysis_host_pageable_streamed(enkf_plan* p, const double* X_h, const double* Y_h, const int64_t* idx_h,
+                                    const double* r_h, double* XA_h, enkf_status* st) {
+  const size_t n = (size_t)p->n;
+  const size_t row_bytes = n * sizeof(double);
+  cudaStream_t s = p->hstream;
+  if (!p->hxo) {
+    CUDA_TRY(cudaMalloc(&p->hxo, row_bytes * (size_t)p->n_obs + 16), st);
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hs_in, cudaStreamNonBlocking), st);
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->hs_out, cudaStreamNonBlocking), st);
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_obs, cudaEventDisableTiming), st);
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_anom, cudaEventDisableTiming), st);
+  }
+  CUDA_TRY(ensure_ring(p), st);
+  for (int i = 0; i < 2; ++i)
+    if (!p->oring[i]) {
+      CUDA_TRY(cudaMallocHost(&p->oring[i], p->ring_bytes), st);
+      CUDA_TRY(cudaEventCreateWithFlags(&p->oring_ev[i], cudaEventDisableTiming), st);
+    }
+  struct Drain {
+    cudaStream_t a, b, c;
+    ~Drain() {
+      cudaStreamSynchronize(a);
+      cudaStreamSynchronize(b);
+      cudaStreamSynchronize(c);
+    }
+  } drain{s, p->hs_in, p->hs_out};
+  // host-side phase clock (ENKF_HOST_TRACE=1)
+  const auto t_start = std::chrono::steady_clock::now();
+  auto ms_since = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  };
+  double t_obs = 0, t_T = 0, t_loop = 0, t_memcpy_in = 0, t_wait_slot = 0;
+  // 1. r, idx, Y (ring), the observed rows gathered on the host (ring)
+  CUDA_TRY(cudaMemsetAsync(p->dstatus, 0, sizeof(DevStatus), s), st);
+  CUDA_TRY(copy_h2d(p, p->hr, r_h, sizeof(double) * (size_t)p->n_obs, s), st);
+  CUDA_TRY(copy_h2d(p, p->hidx, idx_h, sizeof(int64_t) * (size_t)p->n_obs, s), st);
+  CUDA_TRY(copy_h2d(p, p->hy, Y_h, row_bytes * (size_t)p->n_obs, s), st);
+  {
+    // index checks the gather relies on (the device re-checks order and range)
+    const int64_t ring_rows = (int64_t)(p->ring_bytes / row_bytes);
+    for (int64_t k0 = 0; k0 < p->n_obs; k0 += ring_rows) {
+      const int64_t rows = std::min<int64_t>(ring_rows, p->n_obs - k0);
+      for (int64_t k = k0; k < k0 + rows; ++k) {
+        if (idx_h[k] < 0 || idx_h[k] >= p->n_state) {
+          set_status(st, ENKF_INDEX_RANGE, "observation index out of range for state size %lld",
+                     (long long)p->n_state);
+          return ENKF_INDEX_RANGE;
+        }
+        if (k > 0 && idx_h[k] <= idx_h[k - 1]) {
+          set_status(st, ENKF_INVALID_ARGUMENT, "indices must be strictly increasing");
+          return ENKF_INVALID_ARGUMENT;
+        }
+      }
+      int slot;
+      CUDA_TRY(take_slot(p, &slot), st);
+      parallel_gather_rows(p->ring[slot], (const char*)X_h, idx_h + k0, rows, row_bytes);
+      CUDA_TRY(cudaMemcpyAsync((char*)p->hxo + (size_t)k0 * row_bytes, p->ring[slot], (size_t)rows * row_bytes,
+                               cudaMemcpyHostToDevice, s), st);
+      CUDA_TRY(cudaEventRecord(p->ring_ev[slot], s), st);
+      p->ring_busy[slot] = true;
+    }
+  }
+  t_obs = ms_since();
+  // 2. Gram on the compact observed rows, levels; the status before any X traffic
+  CUDA_TRY(launch_gram_global(p, p->hxo, p->hy, nullptr, p->hr, s), st);
+  CUDA_TRY(launch_levels(p, p->gram, p->A, p->T, p->den, 1.0 / std::sqrt((double)(p->n - 1)), s), st);
+  {
+    int rc = enkf_plan_sync_status(p, s, st);
+    if (rc != ENKF_OK) return rc;
+  }
+  t_T = ms_since();
+  // 3. X in (inbound ring, hs_in), anomaly per chunk in place (s), X^A out (outbound ring, hs_out)
+  const int64_t chunk_rows = (int64_t)(p->ring_bytes / row_bytes);
+  const int64_t nchunks = (p->n_state + chunk_rows - 1) / chunk_rows;
+  while ((int64_t)p->chunk_ev.size() < nchunks) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
+    p->chunk_ev.push_back(ev);
+  }
+  auto drain_out = [&](int64_t c) -> cudaError_t {
+    const int64_t r0 = c * chunk_rows, rows = std::min<int64_t>(chunk_rows, p->n_state - r0);
+    cudaError_t e = cudaEventSynchronize(p->oring_ev[c & 1]);
+    if (e != cudaSuccess) return e;
+    parallel_memcpy((char*)XA_h + (size_t)r0 * row_bytes, p->oring[c & 1], (size_t)rows * row_bytes);
+    return cudaSuccess;
+  };
+  // (a page-locked X or X^A - e.g. the Python layer's page-locked result arrays - is
+  // DMA'd directly instead of through its ring)
+  const bool x_pinned = is_pinned(X_h), xa_pinned = is_pinned(XA_h);
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t r0 = c * chunk_rows, rows = std::min<int64_t>(chunk_rows, p->n_state - r0);
+    const size_t bytes = (size_t)rows * row_bytes;
+    double* dx = p->hx + (size_t)r0 * n;
+    if (x_pinned) {
+      CUDA_TRY(cudaMemcpyAsync(dx, (const char*)X_h + (size_t)r0 * row_bytes, bytes, cudaMemcpyHostToDevice,
+                               p->hs_in), st);
+    } else {
+      int slot;
+      const double t0 = ms_since();
+      CUDA_TRY(take_slot(p, &slot), st);
+      const double t1 = ms_since();
+      parallel_memcpy(p->ring[slot], (const char*)X_h + (size_t)r0 * row_bytes, bytes);
+      t_wait_slot += t1 - t0;
+      t_memcpy_in += ms_since() - t1;
+      CUDA_TRY(cudaMemcpyAsync(dx, p->ring[slot], bytes, cudaMemcpyHostToDevice, p->hs_in), st);
+      CUDA_TRY(cudaEventRecord(p->ring_ev[slot], p->hs_in), st);
+      p->ring_busy[slot] = true;
+    }
+    CUDA_TRY(cudaEventRecord(p->chunk_ev[c], p->hs_in), st);
+    CUDA_TRY(cudaStreamWaitEvent(s, p->chunk_ev[c], 0), st);
+    CUDA_TRY(launch_rowgemm<0>(p, dx, p->T, nullptr, nullptr, dx, rows, s), st);
+    CUDA_TRY(cudaEventRecord(p->ev_anom, s), st);
+    CUDA_TRY(cudaStreamWaitEvent(p->hs_out, p->ev_anom, 0), st);
+    if (xa_pinned) {
+      CUDA_TRY(cudaMemcpyAsync((char*)XA_h + (size_t)r0 * row_bytes, dx, bytes, cudaMemcpyDeviceToHost, p->hs_out),
+               st);
+    } else {
+      // the outbound slot of chunk c was drained by the host when chunk c - 1 was queued
+      CUDA_TRY(cudaMemcpyAsync(p->oring[c & 1], dx, bytes, cudaMemcpyDeviceToHost, p->hs_out), st);
+      CUDA_TRY(cudaEventRecord(p->oring_ev[c & 1], p->hs_out), st);
+      if (c >= 1) CUDA_TRY(drain_out(c - 1), st);
+    }
+  }
+  if (!xa_pinned && nchunks >= 1) CUDA_TRY(drain_out(nchunks - 1), st);
+  t_loop = ms_since();
+  CUDA_TRY(cudaStreamSynchronize(p->hs_out), st);
+  if (p->host_trace)
+    fprintf(stderr,
+            "[enkf host pageable] obs side queued %.1f ms, T ready %.1f ms, X loop queued %.1f ms (slot waits %.1f, "
+            "host copies in %.1f), X^A out done %.1f ms\n",
+            t_obs, t_T, t_loop, t_wait_slot, t_memcpy_in, ms_since());
+  CUDA_TRY(cudaStreamSynchronize(s), st);
+  return ENKF_OK;
+}
 }  // namespace
 
 int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_h,
@@ -1138,6 +1316,8 @@ int32_t enkf_analysis_host_f64(enkf_plan* p, const double* X_h, const double* Y_
     const void* Xmap = mapped_device_ptr(X_h);
     if (Xmap && is_pinned(XA_h))
       return analysis_host_streamed(p, X_h, (const double*)Xmap, Y_h, idx_h, r_h, XA_h, st);
+    if (sizeof(double) * (size_t)p->n_state * n >= p->pageable_stream_min)
+      return analysis_host_pageable_streamed(p, X_h, Y_h, idx_h, r_h, XA_h, st);
   }
   struct Drain {
     cudaStream_t a;

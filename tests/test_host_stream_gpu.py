@@ -129,3 +129,59 @@ def test_streamed_path_errors(monkeypatch):
     rc, st = _host_call(plan, x, y, good, r, out)
     assert rc == 0, st.message
     assert rel_err(out, oracle.analysis_step(np.array(x), np.array(y), good, r)) <= 1e-9
+
+
+@pytest.mark.parametrize("xa_pinned", [False, True])
+def test_pageable_streamed_equals_device(xa_pinned, monkeypatch):
+    """The pageable form of the streamed host path (the caller's ordinary arrays:
+    observed rows gathered on the host, X in and X^A out through pinned rings while
+    the anomaly update runs chunk by chunk): 1 MiB ring slots give 1024-row chunks,
+    the last one ragged; bit-equal to the device-resident step, with a pageable or a
+    page-locked X^A."""
+    import torch
+    p = W.config4(8)
+    x = np.array(p.x[:-333])  # 65203 rows: 63 full 1024-row chunks and a ragged one
+    idx = np.ascontiguousarray(p.indices, dtype=np.int64)
+    keep = idx < x.shape[0]
+    idx, y, r = idx[keep], np.ascontiguousarray(p.perturbed[keep]), np.ascontiguousarray(p.r[keep])
+    out = _pinned(np.zeros_like(x)) if xa_pinned else np.zeros_like(x)
+    plan = _plan((x.shape[0], idx.size, x.shape[1]), monkeypatch, ENKF_HOST_STREAM_MIN_MB="0", ENKF_HOST_RING_MB="1")
+    rc, st = _host_call(plan, x, y, idx, r, out)
+    assert rc == 0, st.message
+    dev = torch.device("cuda", 0)
+    obs = P.ObservationBatch(y=None, perturbed=torch.from_numpy(y).to(dev), perturbations=None)
+    xa_d = P.analysis_step(torch.from_numpy(x).to(dev), obs, P.SelectionOperator.from_indices(idx),
+                           torch.from_numpy(r).to(dev))
+    assert np.array_equal(xa_d.cpu().numpy(), out)
+    assert rel_err(out, oracle.analysis_step(x, y, idx, r)) <= 1e-9
+
+
+def test_pageable_streamed_errors(monkeypatch):
+    """Index range / order (checked on the host before the gather) and non-finite /
+    non-positive inputs (device flags) through the pageable streamed path."""
+    rng = np.random.default_rng(7)
+    ns, nobs, n = 6000, 700, 128
+    x = rng.standard_normal((ns, n))
+    y = rng.standard_normal((nobs, n))
+    r = np.ones(nobs)
+    good = np.sort(rng.choice(ns, nobs, replace=False)).astype(np.int64)
+    plan = _plan((ns, nobs, n), monkeypatch, ENKF_HOST_STREAM_MIN_MB="0", ENKF_HOST_RING_MB="1")
+    out = np.zeros((ns, n))
+    bad_range = good.copy()
+    bad_range[-1] = ns + 10**9  # must not be read
+    bad_order = good.copy()
+    bad_order[5] = bad_order[4]
+    for idx, code in ((bad_range, _native.ENKF_INDEX_RANGE), (bad_order, _native.ENKF_INVALID_ARGUMENT)):
+        rc, st = _host_call(plan, x, y, idx, r, out)
+        assert rc == code, st.message
+    r_bad = r.copy()
+    r_bad[3] = -1.0
+    rc, st = _host_call(plan, x, y, good, r_bad, out)
+    assert rc == _native.ENKF_INVALID_ARGUMENT and b"positive" in st.message
+    x_nan = x.copy()
+    x_nan[good[17], 3] = np.nan
+    rc, st = _host_call(plan, x_nan, y, good, r, out)
+    assert rc == _native.ENKF_INVALID_ARGUMENT and b"non-finite" in st.message
+    rc, st = _host_call(plan, x, y, good, r, out)
+    assert rc == 0, st.message
+    assert rel_err(out, oracle.analysis_step(x, y, good, r)) <= 1e-9
