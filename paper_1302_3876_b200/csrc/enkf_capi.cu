@@ -20,7 +20,6 @@
 #include "localized.cuh"
 #include "l96.cuh"
 #include "gram_i8.cuh"
-#include "gram_i8_fused.cuh"
 #include "host_stream.cuh"
 #include "tiny.cuh"
 #include "nccl_comm.cuh"
@@ -46,7 +45,6 @@ struct enkf_plan {
   bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
-  bool gram_fused = false;                // one persistent slice+MMA kernel (opt-in: ENKF_GRAM=i8fused)
   double* g8_ls_partial = nullptr;        // [groups][4][256][128] (level-split form)
   int* g8_ls_progress = nullptr;          // [groups][4] blocks issued per CTA (level-split pacing)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
@@ -56,8 +54,6 @@ struct enkf_plan {
   bool g8_events = false;                 // measurement: events around the slice and MMA passes
   cudaEvent_t g8_ev[3] = {nullptr, nullptr, nullptr};
   unsigned char* g8_planes = nullptr;     // [ceil(n_obs/32)][48 KiB] digit-plane operand images (two-kernel form)
-  unsigned char* g8_ring = nullptr;       // [groups][GF_RING][48 KiB] L2-resident image ring (fused form)
-  int* g8_flags = nullptr;                // [2][groups][GF_RING] ready / consumed counters
   unsigned long long* g8_meta = nullptr;  // [256] sampled column maxima, then the overflow flag
   int ws_blocks = 1, ws_ctas_per_block = 1;
   int64_t ws_rows_per_cta = 0;
@@ -234,19 +230,13 @@ cudaError_t ensure_gram_i8_workspace(enkf_plan* p) {
   const int64_t n_blocks = (p->n_obs + G8_KB - 1) / G8_KB;
   if (!p->g8_meta && (e = cudaMalloc(&p->g8_meta, sizeof(unsigned long long) * (2 * G8_N + 2))) != cudaSuccess)
     return e;
-  if (p->gram_fused) {  // L2-resident per-group image rings + their ready / consumed counters
-    if (!p->g8_ring && (e = cudaMalloc(&p->g8_ring, (size_t)p->g8_groups * GFL_RING * G8LS_STAGE)) != cudaSuccess)
-      return e;
-    if (!p->g8_flags && (e = cudaMalloc(&p->g8_flags, sizeof(int) * 2 * p->g8_groups * GFL_RING)) != cudaSuccess)
-      return e;
-  } else if (!p->g8_planes && n_blocks > 0 &&
-             (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess) {
+  if (!p->g8_planes && n_blocks > 0 &&
+      (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess)
     return e;
-  }
   if (!p->g8_ls_partial &&
       (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
     return e;
-  if (!p->gram_fused && !p->g8_ls_progress &&
+  if (!p->g8_ls_progress &&
       (e = cudaMalloc(&p->g8_ls_progress, sizeof(int) * 4 * p->g8_groups)) != cudaSuccess)
     return e;
   return cudaSuccess;
@@ -265,59 +255,29 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
   if ((e = cudaMemsetAsync(p->g8_meta, 0, sizeof(unsigned long long) * (2 * G8_N + 2), s)) != cudaSuccess) return e;
   gram_i8_scales_kernel<<<p->num_sms * 2, 256, 0, s>>>(X, Y, idx, r, p->n_state, p->n_obs, p->g8_meta);
   const int64_t bpg = (n_blocks + p->g8_groups - 1) / p->g8_groups;
-  if (p->gram_fused) {
-    const size_t nflags = (size_t)2 * p->g8_groups * GFL_RING;
-    if ((e = cudaMemsetAsync(p->g8_flags, 0, sizeof(int) * nflags, s)) != cudaSuccess) return e;
-    const size_t smem = gram_i8_fused_smem_bytes();
-    if ((e = cudaFuncSetAttribute(gram_i8_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    int* ready = p->g8_flags;
-    int* consumed = p->g8_flags + (size_t)p->g8_groups * GFL_RING;
-    int64_t n_state = p->n_state, n_obs = p->n_obs, nb = n_blocks, bpg_v = bpg;
-    const unsigned long long* cmax = p->g8_meta;
-    double* partial = p->g8_ls_partial;
-    DevStatus* dstatus = p->dstatus;
-    unsigned char* ring = p->g8_ring;
-    void* args[] = {(void*)&X, (void*)&Y, (void*)&idx, (void*)&r, (void*)&cmax, (void*)&n_state, (void*)&n_obs,
-                    (void*)&nb, (void*)&bpg_v, (void*)&ring, (void*)&ready, (void*)&consumed, (void*)&partial,
-                    (void*)&overflow, (void*)&dstatus};
-    if (p->g8_events) {
-      for (cudaEvent_t& ev : p->g8_ev)
-        if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
-      cudaEventRecord(p->g8_ev[0], s);
-      cudaEventRecord(p->g8_ev[1], s);
-    }
-    // cooperative: every CTA co-resident (they wait on each other through the ring)
-    e = cudaLaunchCooperativeKernel((const void*)gram_i8_fused_kernel, dim3(4 * p->g8_groups), dim3(GFL_THREADS),
-                                    args, smem, s);
-    if (e != cudaSuccess) return e;
-    if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
-  } else {
-    if (p->g8_events) {
-      for (cudaEvent_t& ev : p->g8_ev)
-        if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
-      cudaEventRecord(p->g8_ev[0], s);
-    }
-    const size_t smem = gram_i8_slice_smem_bytes();
-    if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    // 2 CTAs per SM are resident (120 registers x 256 threads): one full wave, no tail
-    const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * G8_SLICE_CTAS_PER_SM);
-    gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
-                                                                         p->n_obs, n_blocks, p->g8_planes, overflow,
-                                                                         p->dstatus);
-    if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
-    const size_t lsmem = gram_i8_ls_smem_bytes();
-    if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem)) !=
-        cudaSuccess)
-      return e;
-    if ((e = cudaMemsetAsync(p->g8_ls_progress, 0, sizeof(int) * 4 * p->g8_groups, s)) != cudaSuccess) return e;
-    gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, lsmem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
-                                                                        p->g8_ls_partial, overflow, p->g8_ls_progress);
-    if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
+  if (p->g8_events) {
+    for (cudaEvent_t& ev : p->g8_ev)
+      if (!ev && (e = cudaEventCreate(&ev)) != cudaSuccess) return e;
+    cudaEventRecord(p->g8_ev[0], s);
   }
+  const size_t smem = gram_i8_slice_smem_bytes();
+  if ((e = cudaFuncSetAttribute(gram_i8_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+      cudaSuccess)
+    return e;
+  // 2 CTAs per SM are resident (120 registers x 256 threads): one full wave, no tail
+  const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * G8_SLICE_CTAS_PER_SM);
+  gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
+                                                                       p->n_obs, n_blocks, p->g8_planes, overflow,
+                                                                       p->dstatus);
+  if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
+  const size_t lsmem = gram_i8_ls_smem_bytes();
+  if ((e = cudaFuncSetAttribute(gram_i8_mma_ls_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(p->g8_ls_progress, 0, sizeof(int) * 4 * p->g8_groups, s)) != cudaSuccess) return e;
+  gram_i8_mma_ls_kernel<<<4 * p->g8_groups, G8LS_THREADS, lsmem, s>>>(p->g8_planes, p->g8_meta, n_blocks, bpg,
+                                                                      p->g8_ls_partial, overflow, p->g8_ls_progress);
+  if (p->g8_events) cudaEventRecord(p->g8_ev[2], s);
   const double svv = 1.0 / (double)(n - 1), svd = 1.0 / std::sqrt((double)(n - 1));
   gram_i8_ls_reduce<<<(2 * G8_N * G8_N + 255) / 256, 256, 0, s>>>(p->g8_ls_partial, p->g8_groups, svv, svd, overflow,
                                                                   gram);
@@ -772,7 +732,6 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   }
   if (const char* env = getenv("ENKF_GRAM")) {
     p->gram_i8 = (strcmp(env, "fp64") != 0);
-    p->gram_fused = (strcmp(env, "i8fused") == 0);
   }
   if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
   if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
@@ -866,10 +825,8 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->locZ);
   cudaFree(p->l96ws);
   cudaFree(p->g8_planes);
-  cudaFree(p->g8_ring);
   for (cudaEvent_t ev : p->g8_ev)
     if (ev) cudaEventDestroy(ev);
-  cudaFree(p->g8_flags);
   cudaFree(p->g8_meta);
   cudaFree(p->g8_ls_partial);
   cudaFree(p->g8_ls_progress);
@@ -1697,9 +1654,6 @@ __attribute__((visibility("default"))) int32_t enkf_debug_lv_trace(long long* ou
 }
 // Profiling-only (not part of include/enkf_b200.h): CTA-0 event trace of the
 // int8 anomaly kernel, filled when ENKF_I8_DBG has bit 3 set.
-__attribute__((visibility("default"))) int32_t enkf_debug_gfl_trace(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, enkf::g_gfl_trace, sizeof(enkf::g_gfl_trace)) == cudaSuccess ? 0 : 5;
-}
 __attribute__((visibility("default"))) int32_t enkf_debug_i8_trace(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, enkf::g_i8_trace, sizeof(enkf::g_i8_trace)) == cudaSuccess ? 0 : 5;
 }

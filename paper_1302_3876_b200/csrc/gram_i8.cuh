@@ -23,7 +23,7 @@
 //    every 512 blocks (16384 rows, where the int32 levels are still exact) 4 flush
 //    warps fold the levels into the fp64 partial.  No FP64 arithmetic runs next to the
 //    MMAs (on B200 it stalls the tensor pipe, anomaly_i8.cuh).
-// gram_i8_fused.cuh holds an opt-in one-kernel form of the same products.
+// (One-kernel forms that keep the images in L2 were built and measured slower.)
 // Any overflow -> the FP64 DMMA Gram (gram128_kernel, gated on the flag, same
 // stream) recomputes the Gram: no host round trip, same results contract.
 #pragma once

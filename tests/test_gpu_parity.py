@@ -502,7 +502,7 @@ np.save(sys.argv[2], gram.cpu().numpy())
     return np.load(out)
 
 
-@pytest.mark.parametrize("mode", ["i8fused", "i8ls"])
+@pytest.mark.parametrize("mode", ["i8ls"])
 @pytest.mark.parametrize("heavy", [0, 1, 2])
 def test_int8_gram_matches_fp64_gram(heavy, mode):
     """The exact-digit tcgen05 Gram (default for N = 128) agrees with the FP64 DMMA
@@ -510,8 +510,7 @@ def test_int8_gram_matches_fp64_gram(heavy, mode):
     sampled scales (1), or one at the top edge of the digit range (2), takes the
     device-gated FP64 fallback (then the two are identical).  "i8ls" is the default
     two-kernel form (slice pass + level-split MMA pass: N = 256 MMAs, A from shared
-    memory), "i8fused" the opt-in one-kernel form (slicers and MMAs in one cooperative
-    launch, images through an L2-resident ring)."""
+    memory)."""
     a, b = _gram_with("fp64", heavy), _gram_with(mode, heavy)
     assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
     tol = 0.0 if heavy else 1e-13
@@ -526,18 +525,6 @@ def test_int8_gram_level_split_mid_size():
     a, b = _gram_with("fp64", 0, 21, 20), _gram_with("i8ls", 0, 21, 20)
     assert np.abs(b[:, :128] - b[:, :128].T).max() == 0.0
     assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
-
-
-@pytest.mark.parametrize("sizes", [(17, 15), (21, 20), (17, 10)])
-def test_fused_gram_equals_two_kernel_gram(sizes):
-    """The one-kernel Gram (slicers and level-split MMAs on the same SMs, images
-    through an L2-resident ring) performs the same exact digit products in the same
-    order as the two-kernel form: the two Grams are identical bit for bit (2^15 rows:
-    < 1 block per CTA; 2^20: multi-period flush, ring wrap; 2^13: groups without
-    blocks)."""
-    a = _gram_with("i8ls", 0, *sizes)
-    b = _gram_with("i8fused", 0, *sizes)
-    assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("n", [2, 5, 8, 20, 31, 64, 96, 97, 127, 128])

@@ -1,7 +1,7 @@
 """A/B of the Gram forms at config 5 (or 2^-s of it): the Gram alone and the whole
 step, per ENKF_GRAM mode, alternating, CUDA events; Grams compared bitwise.
 
-    python tools/probe/gram_ab.py [scale_log2] [modes, e.g. i8ls,i8fused,i8ls:1024] [reps]
+    python tools/probe/gram_ab.py [scale_log2] [modes, e.g. i8ls,fp64] [reps]
 """
 import ctypes
 import json
@@ -16,7 +16,7 @@ from paper_1302_3876_b200 import _native  # noqa: E402
 from paper_1302_3876_b200 import workloads as W  # noqa: E402
 
 scale = int(sys.argv[1]) if len(sys.argv) > 1 else 0
-modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["i8ls", "i8fused"]
+modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["i8ls", "fp64"]
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
 dev = torch.device("cuda", 0)
 lib = _native.lib()
@@ -26,12 +26,9 @@ x, y, idx, r = d["x"], d["perturbed"], d["idx"], d["r"]
 ns, no, n = x.shape[0], y.shape[0], x.shape[1]
 xa = torch.empty_like(x)
 plans = {}
-for m in modes:  # "mode" or "mode:chunk_blocks" (ENKF_GRAM_CHUNK)
-    os.environ["ENKF_GRAM"] = m.split(":")[0]
-    if ":" in m:
-        os.environ["ENKF_GRAM_CHUNK"] = m.split(":")[1]
+for m in modes:
+    os.environ["ENKF_GRAM"] = m
     plans[m] = _native.Plan(ns, no, n, 0)
-    os.environ.pop("ENKF_GRAM_CHUNK", None)
 os.environ.pop("ENKF_GRAM", None)
 gram = {m: torch.empty((n, 2 * n), dtype=torch.float64, device=dev) for m in modes}
 res = {m: {"gram_ms": [], "step_ms": []} for m in modes}
