@@ -96,6 +96,34 @@ int32_t enkf_get_device(int32_t* device);
  * device before returning.  Thread-safe per plan (one call at a time). */
 int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens,
                          enkf_plan** plan, enkf_status* status);
+
+/* Kernel and host-path choices of a plan (the reference has no counterpart: its
+ * module constants GROUP_LEVELS / SINGULAR_TOL are fixed, sherman.py:51, 146).
+ * enkf_plan_options_default() fills the product defaults, then applies the
+ * process-wide ENKF_* environment overrides;
+ * enkf_plan_create(...) == enkf_plan_create_ex(..., NULL, ...) uses exactly that.
+ * Every choice computes the same analysis within the parity tolerance; they exist
+ * for A/B measurement and for callers that require IEEE FP64 arithmetic. */
+enum enkf_gram_kernel { ENKF_GRAM_INT8 = 0 /* exact int8-digit tcgen05 (N = 128) */, ENKF_GRAM_FP64 = 1 /* DMMA */ };
+enum enkf_anomaly_kernel { ENKF_ANOMALY_INT8 = 0, ENKF_ANOMALY_FP64 = 1 };
+enum enkf_levels_kernel { ENKF_LEVELS_CLUSTER = 0, ENKF_LEVELS_SINGLE_CTA = 1, ENKF_LEVELS_PER_LEVEL = 2 };
+typedef struct enkf_plan_options {
+  int32_t struct_size;        /* sizeof(enkf_plan_options): set by enkf_plan_options_default */
+  int32_t gram_kernel;        /* enum enkf_gram_kernel */
+  int32_t anomaly_kernel;     /* enum enkf_anomaly_kernel */
+  int32_t levels_kernel;      /* enum enkf_levels_kernel */
+  int32_t localized_dmma;     /* 1: DMMA localized update (default), 0: CUDA-core form */
+  int32_t tiny_kernel;        /* 1: single-CTA step for desk-scale shapes (default), 0: multi-kernel */
+  int32_t host_stream;        /* 1: streamed host entry (default), 0: copy in / step / copy out */
+  int32_t host_trace;         /* 1: phase times of the host entry on stderr */
+  int64_t host_chunk_bytes;   /* X / XA chunk of the streamed host entry (default 256 MiB) */
+  int64_t host_ring_bytes;    /* pinned staging-ring slot for pageable buffers (default 256 MiB) */
+  int64_t host_stream_min_bytes; /* pageable X from this size streams through the rings (default 1 GiB) */
+} enkf_plan_options;
+int32_t enkf_plan_options_default(enkf_plan_options* options);
+int32_t enkf_plan_create_ex(int64_t n_state, int64_t n_obs, int64_t n_ens,
+                            const enkf_plan_options* options /* NULL = defaults */,
+                            enkf_plan** plan, enkf_status* status);
 void enkf_plan_destroy(enkf_plan* plan);
 
 /* Full analysis step on device buffers (single GPU or one shard whose obs rows

@@ -36,10 +36,28 @@ class EnkfStatus(ctypes.Structure):
     ]
 
 
+class EnkfPlanOptions(ctypes.Structure):
+    """enkf_plan_options (include/enkf_b200.h): kernel and host-path choices of a plan."""
+    _fields_ = [
+        ("struct_size", ctypes.c_int32),
+        ("gram_kernel", ctypes.c_int32),      # 0 int8-digit tcgen05, 1 FP64 DMMA
+        ("anomaly_kernel", ctypes.c_int32),   # 0 int8-digit tcgen05, 1 FP64 DMMA
+        ("levels_kernel", ctypes.c_int32),    # 0 cluster, 1 single CTA, 2 level by level
+        ("localized_dmma", ctypes.c_int32),
+        ("tiny_kernel", ctypes.c_int32),
+        ("host_stream", ctypes.c_int32),
+        ("host_trace", ctypes.c_int32),
+        ("host_chunk_bytes", ctypes.c_int64),
+        ("host_ring_bytes", ctypes.c_int64),
+        ("host_stream_min_bytes", ctypes.c_int64),
+    ]
+
+
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
 _st = ctypes.POINTER(EnkfStatus)
+_opt = ctypes.POINTER(EnkfPlanOptions)
 
 # name -> (restype, argtypes); must match include/enkf_b200.h exactly.
 PROTOTYPES = {
@@ -49,6 +67,8 @@ PROTOTYPES = {
     "enkf_get_device": (_i32, [ctypes.POINTER(_i32)]),
     "enkf_plan_reset_status": (_i32, [_vp, _vp]),
     "enkf_plan_create": (_i32, [_i64, _i64, _i64, ctypes.POINTER(_vp), _st]),
+    "enkf_plan_options_default": (_i32, [_opt]),
+    "enkf_plan_create_ex": (_i32, [_i64, _i64, _i64, _opt, ctypes.POINTER(_vp), _st]),
     "enkf_plan_destroy": (None, [_vp]),
     "enkf_analysis_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _st]),
     "enkf_analysis_async_f64": (_i32, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -155,18 +175,35 @@ class on_device:
         return False
 
 
+def default_options() -> EnkfPlanOptions:
+    """Product defaults with the ENKF_* environment overrides applied."""
+    o = EnkfPlanOptions()
+    if lib().enkf_plan_options_default(ctypes.byref(o)) != ENKF_OK:
+        raise RuntimeError("enkf_plan_options_default failed")
+    return o
+
+
 class Plan:
     """Owns one enkf_plan (device workspace for a fixed shape)."""
 
-    def __init__(self, n_state: int, n_obs: int, n_ens: int, device_index: int = 0):
+    def __init__(self, n_state: int, n_obs: int, n_ens: int, device_index: int = 0, options: dict | None = None):
+        """`options`: enkf_plan_options fields to change from the defaults (which
+        include the process-wide ENKF_* environment overrides), e.g.
+        {"gram_kernel": 1, "anomaly_kernel": 1} for the all-IEEE-FP64 step."""
         self.shape = (int(n_state), int(n_obs), int(n_ens))
         self.device_index = int(device_index)
         self._h = _vp()
         st = EnkfStatus()
+        opts = default_options()
+        for k, v in (options or {}).items():
+            if k not in dict(EnkfPlanOptions._fields_) or k == "struct_size":
+                raise ValueError(f"unknown plan option {k!r}")
+            setattr(opts, k, int(v))
+        self.options = opts
         with on_device(self.device_index):
-            code = lib().enkf_plan_create(self.shape[0], self.shape[1], self.shape[2],
-                                          ctypes.byref(self._h), ctypes.byref(st))
-        raise_for_status(code, st, "enkf_plan_create")
+            code = lib().enkf_plan_create_ex(self.shape[0], self.shape[1], self.shape[2], ctypes.byref(opts),
+                                             ctypes.byref(self._h), ctypes.byref(st))
+        raise_for_status(code, st, "enkf_plan_create_ex")
         self.lock = threading.Lock()
 
     @property

@@ -662,8 +662,62 @@ int32_t enkf_get_device(int32_t* device) {
   return ENKF_OK;
 }
 
+int32_t enkf_plan_options_default(enkf_plan_options* o) {
+  if (!o) return ENKF_INVALID_ARGUMENT;
+  memset(o, 0, sizeof(*o));
+  o->struct_size = (int32_t)sizeof(*o);
+  o->gram_kernel = ENKF_GRAM_INT8;
+  o->anomaly_kernel = ENKF_ANOMALY_INT8;
+  o->levels_kernel = ENKF_LEVELS_CLUSTER;
+  o->localized_dmma = 1;
+  o->tiny_kernel = 1;
+  o->host_stream = 1;
+  o->host_trace = 0;
+  o->host_chunk_bytes = (int64_t)256 << 20;
+  o->host_ring_bytes = (int64_t)256 << 20;
+  o->host_stream_min_bytes = (int64_t)1 << 30;
+  // process-wide overrides (A/B measurements without recompiling the caller)
+  if (const char* env = getenv("ENKF_GRAM")) o->gram_kernel = strcmp(env, "fp64") == 0 ? ENKF_GRAM_FP64 : ENKF_GRAM_INT8;
+  if (const char* env = getenv("ENKF_ANOMALY"))
+    o->anomaly_kernel = strcmp(env, "fp64") == 0 ? ENKF_ANOMALY_FP64 : ENKF_ANOMALY_INT8;
+  if (const char* env = getenv("ENKF_LEVELS"))
+    o->levels_kernel = strcmp(env, "level") == 0    ? ENKF_LEVELS_PER_LEVEL
+                       : strcmp(env, "single") == 0 ? ENKF_LEVELS_SINGLE_CTA
+                                                    : ENKF_LEVELS_CLUSTER;
+  if (const char* env = getenv("ENKF_LOCALIZED")) o->localized_dmma = strcmp(env, "fma") != 0;
+  if (const char* env = getenv("ENKF_TINY")) o->tiny_kernel = env[0] != '0';
+  if (const char* env = getenv("ENKF_HOST_STREAM")) o->host_stream = env[0] != '0';
+  if (const char* env = getenv("ENKF_HOST_TRACE")) o->host_trace = env[0] == '1';
+  if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) o->host_chunk_bytes = (int64_t)atol(env) << 20;
+  if (const char* env = getenv("ENKF_HOST_STREAM_MIN_MB")) o->host_stream_min_bytes = (int64_t)atol(env) << 20;
+  if (const char* env = getenv("ENKF_HOST_RING_MB")) {
+    const int64_t mb = atol(env);
+    o->host_ring_bytes = (mb > 0 ? mb : 1) << 20;
+  }
+  return ENKF_OK;
+}
+
 int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_plan** out,
                          enkf_status* st) {
+  return enkf_plan_create_ex(n_state, n_obs, n_ens, nullptr, out, st);
+}
+
+int32_t enkf_plan_create_ex(int64_t n_state, int64_t n_obs, int64_t n_ens, const enkf_plan_options* options,
+                            enkf_plan** out, enkf_status* st) {
+  enkf_plan_options opt;
+  enkf_plan_options_default(&opt);
+  if (options) {
+    if (options->struct_size != (int32_t)sizeof(enkf_plan_options) || options->gram_kernel < 0 ||
+        options->gram_kernel > ENKF_GRAM_FP64 || options->anomaly_kernel < 0 ||
+        options->anomaly_kernel > ENKF_ANOMALY_FP64 || options->levels_kernel < 0 ||
+        options->levels_kernel > ENKF_LEVELS_PER_LEVEL || options->host_chunk_bytes <= 0 ||
+        options->host_ring_bytes <= 0 || options->host_stream_min_bytes < 0) {
+      set_status(st, ENKF_INVALID_ARGUMENT, "invalid enkf_plan_options (start from enkf_plan_options_default)");
+      if (out) *out = nullptr;
+      return ENKF_INVALID_ARGUMENT;
+    }
+    opt = *options;
+  }
   if (!out) {
     set_status(st, ENKF_INVALID_ARGUMENT, "null plan pointer");
     return ENKF_INVALID_ARGUMENT;
@@ -722,27 +776,20 @@ int32_t enkf_plan_create(int64_t n_state, int64_t n_obs, int64_t n_ens, enkf_pla
   p->ws_rows_per_cta = rpc;
   if (const char* env = getenv("ENKF_DISABLE_WS")) p->use_ws = (env[0] == '0');
   if (const char* env = getenv("ENKF_DISABLE_G128")) p->use_128 = (env[0] == '0');
-  if (const char* env = getenv("ENKF_ANOMALY")) p->anomaly_i8 = (strcmp(env, "fp64") != 0);
 #ifdef I8_DBG_BUILD  // profiling variants only (tools/build_variant.py NAME -DI8_DBG_BUILD)
   if (const char* env = getenv("ENKF_I8_DBG")) p->i8_dbg = atoi(env);
 #endif
-  if (const char* env = getenv("ENKF_LEVELS")) {
-    p->levels_blocked = (strcmp(env, "level") != 0);
-    p->levels_cluster = (strcmp(env, "level") != 0 && strcmp(env, "single") != 0);
-  }
-  if (const char* env = getenv("ENKF_GRAM")) {
-    p->gram_i8 = (strcmp(env, "fp64") != 0);
-  }
-  if (const char* env = getenv("ENKF_HOST_STREAM")) p->host_streamed = (env[0] != '0');
-  if (const char* env = getenv("ENKF_LOCALIZED")) p->loc_dmma = (strcmp(env, "fma") != 0);
-  if (const char* env = getenv("ENKF_TINY")) p->tiny = (env[0] != '0');
-  if (const char* env = getenv("ENKF_HOST_TRACE")) p->host_trace = (env[0] == '1');
-  if (const char* env = getenv("ENKF_HOST_CHUNK_MB")) p->host_chunk_bytes = (size_t)atol(env) << 20;
-  if (const char* env = getenv("ENKF_HOST_STREAM_MIN_MB")) p->pageable_stream_min = (size_t)atol(env) << 20;
-  if (const char* env = getenv("ENKF_HOST_RING_MB")) {
-    const size_t mb = (size_t)atol(env);
-    p->ring_bytes_cfg = (mb > 0 ? mb : 1) << 20;
-  }
+  p->gram_i8 = opt.gram_kernel == ENKF_GRAM_INT8;
+  p->anomaly_i8 = opt.anomaly_kernel == ENKF_ANOMALY_INT8;
+  p->levels_blocked = opt.levels_kernel != ENKF_LEVELS_PER_LEVEL;
+  p->levels_cluster = opt.levels_kernel == ENKF_LEVELS_CLUSTER;
+  p->loc_dmma = opt.localized_dmma != 0;
+  p->tiny = opt.tiny_kernel != 0;
+  p->host_streamed = opt.host_stream != 0;
+  p->host_trace = opt.host_trace != 0;
+  p->host_chunk_bytes = (size_t)opt.host_chunk_bytes;
+  p->pageable_stream_min = (size_t)opt.host_stream_min_bytes;
+  p->ring_bytes_cfg = (size_t)opt.host_ring_bytes;
   p->g8_groups = p->num_sms / 4 > 0 ? p->num_sms / 4 : 1;
 
   // gram128 split: the V'V CTAs do 3/4 of the DMMA work of the V'D CTAs (and

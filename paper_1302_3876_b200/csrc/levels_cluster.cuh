@@ -10,8 +10,11 @@
 //  * every CTA factors the (identical) pivot block itself, solves Q for its own
 //    columns and updates them;
 //  * the next block's pivot columns P = Gamma[:, K'] are pushed by the owners of the
-//    entries into every CTA's (double-buffered) P buffer through distributed shared
-//    memory, then one cluster barrier per block.
+//    entries into every CTA's P buffer through distributed shared memory, then one
+//    cluster barrier per block.  The P buffer is triple-buffered: a CTA still reads
+//    P(blk) in its V'D update after it has arrived at block blk's barrier, and a faster
+//    CTA that has passed that barrier pushes P(blk + 2) during block blk + 1 — into a
+//    third buffer, so no push can land in a buffer that is still being read.
 // CTA 0 reports the singular guard / den_k; A and T leave straight from the
 // fragments (column means in a fixed order).
 #pragma once
@@ -40,7 +43,7 @@ __host__ __device__ inline int lc_vv_doubles(int n) {
 }
 __host__ __device__ inline int64_t levels_cluster_smem_doubles(int n) {
   const int mmax = lc_cols(n, 0);
-  return (int64_t)lc_vv_doubles(n) + 2 * LB * (int64_t)n /*PT x2*/ + LB * (int64_t)(mmax + 1) /*Rv/Qv*/ +
+  return (int64_t)lc_vv_doubles(n) + 3 * LB * (int64_t)n /*PT x3*/ + LB * (int64_t)(mmax + 1) /*Rv/Qv*/ +
          LB * 32 /*Rd/Qd*/ + LB * LB /*L*/ + 2 * LB /*D, 1/D*/ + 4 * 32 /*column partials*/ + 32 /*colmean*/ + 8;
 }
 
@@ -71,8 +74,8 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
   const int mown = lc_cols(n, r), mmax = lc_cols(n, 0);
   const int w = lc_w(n), cd0 = r * w;  // V'D columns [cd0, cd0 + w) of this CTA
   double* vv = csm;                                        // own V'V columns, packed
-  double* PTb = vv + lc_vv_doubles(n);                     // [2][LB][n] pivot columns, double-buffered
-  double* Rv = PTb + 2 * LB * n;                           // [LB][mmax + 1] R, then Q (own V'V columns)
+  double* PTb = vv + lc_vv_doubles(n);                     // [3][LB][n] pivot columns, triple-buffered
+  double* Rv = PTb + 3 * LB * n;                           // [LB][mmax + 1] R, then Q (own V'V columns)
   double* Rd = Rv + LB * (mmax + 1);                       // [LB][32]       R, then Q (own V'D columns)
   double* Lm = Rd + LB * 32;                               // [LB][LB]
   double* Dm = Lm + LB * LB;                               // [2 LB]
@@ -91,6 +94,7 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
     const int j = e / n, i = e - j * n;
     PTb[e] = (j < n) ? (i <= j ? gram[(int64_t)i * n2 + j] : gram[(int64_t)j * n2 + i]) : 0.0;
     PTb[LB * n + e] = 0.0;  // rows of a short last block are never pushed: keep them finite
+    PTb[2 * LB * n + e] = 0.0;
   }
   // V'D fragments: warp (wm, wn) owns rows 32 wm.., columns cd0 + (w/2) wn + 8 nt
   const int wm = warp & 3, wn = warp >> 2, fr = lane >> 2, fk = lane & 3;
@@ -137,8 +141,8 @@ ism_levels_cluster_kernel(const double* __restrict__ gram, int n, double cscale,
   for (int k0 = 0, blk = 0; k0 < n; k0 += LB, ++blk) {
     const int b = (n - k0) < LB ? (n - k0) : LB;
     const int c0 = k0 + b;
-    const double* PT = PTb + (blk & 1) * LB * n;
-    double* PTn = PTb + ((blk + 1) & 1) * LB * n;
+    const double* PT = PTb + (blk % 3) * LB * n;
+    double* PTn = PTb + ((blk + 1) % 3) * LB * n;
     if (r == 0) LV_TRACE(blk, 0);
     // (1. R for this block was gathered at the end of the previous one)
     // ---- 2. LDL' of M = I + Gamma[K, K] (every CTA the same), one thread in registers

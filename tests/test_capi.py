@@ -77,3 +77,41 @@ def test_sm100a_sass_present():
         body = [b for n, b in funcs.items() if kern in n]
         assert body and "DMMA.8x8x4" in body[0], kern
 
+
+
+def test_plan_options_defaults_and_env_overrides(so, monkeypatch):
+    """enkf_plan_options_default: product defaults (int8-digit Gram and anomaly
+    kernels, cluster levels, streamed host entry, 256 MiB chunks), with the
+    process-wide ENKF_* environment overrides applied on top (no GPU needed)."""
+    for k in ("ENKF_GRAM", "ENKF_ANOMALY", "ENKF_LEVELS", "ENKF_HOST_RING_MB", "ENKF_TINY", "ENKF_HOST_STREAM"):
+        monkeypatch.delenv(k, raising=False)
+    o = _native.default_options()
+    assert o.struct_size == ctypes.sizeof(_native.EnkfPlanOptions)
+    assert (o.gram_kernel, o.anomaly_kernel, o.levels_kernel) == (0, 0, 0)
+    assert (o.localized_dmma, o.tiny_kernel, o.host_stream, o.host_trace) == (1, 1, 1, 0)
+    assert o.host_chunk_bytes == 256 << 20 and o.host_ring_bytes == 256 << 20
+    assert o.host_stream_min_bytes == 1 << 30
+    monkeypatch.setenv("ENKF_GRAM", "fp64")
+    monkeypatch.setenv("ENKF_ANOMALY", "fp64")
+    monkeypatch.setenv("ENKF_LEVELS", "single")
+    monkeypatch.setenv("ENKF_HOST_RING_MB", "1")
+    o = _native.default_options()
+    assert (o.gram_kernel, o.anomaly_kernel, o.levels_kernel) == (1, 1, 1)
+    assert o.host_ring_bytes == 1 << 20
+    assert _native.lib().enkf_plan_options_default(None) == _native.ENKF_INVALID_ARGUMENT
+
+
+def test_plan_create_ex_rejects_bad_options(so):
+    """Argument validation happens before any CUDA call: a struct that did not come
+    from enkf_plan_options_default, or an out-of-range kernel choice, is
+    ENKF_INVALID_ARGUMENT with a null plan."""
+    lib = _native.lib()
+    for field, value in (("struct_size", 8), ("gram_kernel", 7), ("levels_kernel", -1), ("host_chunk_bytes", 0)):
+        o = _native.default_options()
+        setattr(o, field, value)
+        h, st = ctypes.c_void_p(), _native.EnkfStatus()
+        code = lib.enkf_plan_create_ex(16, 8, 4, ctypes.byref(o), ctypes.byref(h), ctypes.byref(st))
+        assert code == _native.ENKF_INVALID_ARGUMENT and not h.value, field
+        assert b"enkf_plan_options" in st.message
+    with pytest.raises(ValueError):
+        _native.Plan(16, 8, 4, 0, options={"no_such_option": 1})

@@ -429,6 +429,41 @@ def test_tensor_core_anomaly_matches_fp64(maker, monkeypatch):
     assert rel_err(xa_tc, ref) <= XA_TOL
 
 
+def test_plan_options_select_the_kernels(monkeypatch):
+    """enkf_plan_create_ex: the kernel families are plan parameters of the C ABI (the
+    ENKF_* environment variables only set process-wide defaults).  A plan created with
+    {gram_kernel: FP64, anomaly_kernel: FP64} computes bit for bit what a plan created
+    under ENKF_GRAM=fp64 ENKF_ANOMALY=fp64 computes, the single-CTA levels option what
+    the cluster kernel computes, and all of them agree with the default int8-digit
+    plan to fp64 rounding level."""
+    import torch
+    p = W.config4(8)
+    dev = torch.device("cuda", 0)
+    x = torch.from_numpy(p.x).to(dev)
+    y = torch.from_numpy(p.perturbed).to(dev)
+    r = torch.from_numpy(p.r).to(dev)
+    idx = torch.from_numpy(p.indices).to(dev)
+    ns, nobs, n = p.shape
+    for k in ("ENKF_GRAM", "ENKF_ANOMALY", "ENKF_LEVELS"):
+        monkeypatch.delenv(k, raising=False)
+    plan_def = _native.Plan(ns, nobs, n, 0)
+    assert (plan_def.options.gram_kernel, plan_def.options.anomaly_kernel) == (0, 0)
+    plan_opt = _native.Plan(ns, nobs, n, 0, options={"gram_kernel": 1, "anomaly_kernel": 1})
+    plan_lv = _native.Plan(ns, nobs, n, 0, options={"levels_kernel": 1})
+    monkeypatch.setenv("ENKF_GRAM", "fp64")
+    monkeypatch.setenv("ENKF_ANOMALY", "fp64")
+    plan_env = _native.Plan(ns, nobs, n, 0)
+    assert (plan_env.options.gram_kernel, plan_env.options.anomaly_kernel) == (1, 1)
+    _, xa_def = _staged_analysis(plan_def, x, y, idx, r)
+    _, xa_opt = _staged_analysis(plan_opt, x, y, idx, r)
+    _, xa_env = _staged_analysis(plan_env, x, y, idx, r)
+    _, xa_lv = _staged_analysis(plan_lv, x, y, idx, r)
+    assert np.array_equal(xa_opt, xa_env)
+    assert np.array_equal(xa_lv, xa_def)
+    assert not np.array_equal(xa_opt, xa_def)       # different kernels did run
+    assert rel_err(xa_def, xa_opt) <= 1e-11
+
+
 def test_tensor_core_anomaly_zero_spread_and_nonfinite():
     import torch
     dev = torch.device("cuda", 0)
