@@ -1513,6 +1513,26 @@ cudaError_t launch_l96(enkf_plan* p, const double* X, double* Xout, double dt, d
     return X == Xout ? cudaSuccess
                      : cudaMemcpyAsync(Xout, X, sizeof(double) * (size_t)ns * n, cudaMemcpyDeviceToDevice, s);
   }
+  // register path: as few members per CTA as one wave of CTAs allows (the stages are
+  // barrier-latency-bound, so the points per thread set the time), rings <= 8192 points
+  if (ns <= 8 * L96R_THREADS && ns * (int64_t)n < (1ll << 31)) {
+    int mbr = (n + p->num_sms - 1) / p->num_sms;
+    if ((int64_t)mbr * ns > 8 * L96R_THREADS) mbr = (int)(8 * L96R_THREADS / ns);
+    const int len = (int)ns * mbr;
+    const int pt = (len + L96R_THREADS - 1) / L96R_THREADS;
+    const size_t smem = 24 * (size_t)len;
+    const int grid = (n + mbr - 1) / mbr;
+    auto go = [&](auto kern) -> cudaError_t {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, L96R_THREADS, smem, s>>>(X, Xout, (int)ns, n, mbr, half_dt, dt, dt6, forcing, n_steps, p->dstatus);
+      return cudaGetLastError();
+    };
+    if (pt <= 1) return go(l96_rk4_reg_kernel<1>);
+    if (pt <= 2) return go(l96_rk4_reg_kernel<2>);
+    if (pt <= 4) return go(l96_rk4_reg_kernel<4>);
+    return go(l96_rk4_reg_kernel<8>);
+  }
   int mb = (int)std::min<int64_t>((int64_t)(L96_SMEM_MAX / (32 * (size_t)ns)), (int64_t)n);
   if (mb >= 1) {
     const size_t smem = 32 * (size_t)ns * mb;

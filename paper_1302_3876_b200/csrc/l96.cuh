@@ -103,6 +103,97 @@ l96_rk4_smem_kernel(const double* __restrict__ X, double* __restrict__ Xout, int
   }
 }
 
+// Register path (rings of at most L96R_THREADS * PT points per CTA): as the
+// shared-memory path, but a thread owns PT fixed points of the member-interleaved
+// ring ([i][m]: the neighbours of element e are e + mb, e - mb, e - 2 mb, cyclic, so
+// no index division) and keeps their x, accumulator and current stage value in
+// registers; shared memory holds only what neighbours read (x and two stage rings).
+// Stage 3 writes no ring, so the step's final update follows it without a barrier:
+// 4 barriers per RK4 step.  Same operations in the same order: bit-identical.
+constexpr int L96R_THREADS = 1024;
+template <int PT>
+__global__ void __launch_bounds__(L96R_THREADS)
+l96_rk4_reg_kernel(const double* __restrict__ X, double* __restrict__ Xout, int ns, int n, int mb_max,
+                   double half_dt, double dt, double dt6, double forcing, int nsteps, DevStatus* st) {
+  extern __shared__ double l96sm[];
+  const int j0 = blockIdx.x * mb_max;
+  const int mb = min(mb_max, n - j0);
+  const int len = ns * mb;
+  double* xs = l96sm;       // x ring (stage 0 reads neighbours here)
+  double* sa = xs + len;
+  double* sb = sa + len;
+  double xr[PT], ar[PT], cur[PT];
+  int gidx[PT];  // element e = (i, m) -> global offset i n + j0 + m
+#pragma unroll
+  for (int t = 0; t < PT; ++t) {
+    const int e = threadIdx.x + t * L96R_THREADS;
+    xr[t] = 0.0;
+    ar[t] = 0.0;
+    gidx[t] = -1;
+    if (e < len) {
+      const int i = e / mb, m = e - i * mb;
+      gidx[t] = i * n + j0 + m;
+      xr[t] = X[(int64_t)gidx[t]];
+      xs[e] = xr[t];
+    }
+    cur[t] = xr[t];
+  }
+  __syncthreads();
+  const int o1 = mb, o2 = 2 * mb;
+  for (int step = 0; step < nsteps; ++step) {
+    const double* src = xs;
+    double* dst = sa;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+#pragma unroll
+      for (int t = 0; t < PT; ++t) {
+        const int e = threadIdx.x + t * L96R_THREADS;
+        if (e < len) {
+          const int ep1 = e + o1 >= len ? e + o1 - len : e + o1;
+          const int em1 = e - o1 < 0 ? e - o1 + len : e - o1;
+          const int em2 = e - o2 < 0 ? e - o2 + len : e - o2;
+          const double k = l96_tendency(src[ep1], src[em2], src[em1], cur[t], forcing);
+          if (s == 0) {
+            ar[t] = k;
+            cur[t] = __dadd_rn(xr[t], __dmul_rn(half_dt, k));
+            dst[e] = cur[t];
+          } else if (s == 1 || s == 2) {
+            ar[t] = __dadd_rn(ar[t], __dmul_rn(2.0, k));
+            cur[t] = __dadd_rn(xr[t], __dmul_rn(s == 1 ? half_dt : dt, k));
+            dst[e] = cur[t];
+          } else {
+            ar[t] = __dadd_rn(ar[t], k);
+          }
+        }
+      }
+      if (s < 3) __syncthreads();
+      src = dst;
+      dst = (dst == sa) ? sb : sa;
+    }
+    bool bad = false;
+    int bad_m = 0x7fffffff;
+#pragma unroll
+    for (int t = 0; t < PT; ++t) {
+      const int e = threadIdx.x + t * L96R_THREADS;
+      if (e < len) {
+        const double v = __dadd_rn(xr[t], __dmul_rn(dt6, ar[t]));
+        xr[t] = v;
+        cur[t] = v;
+        xs[e] = v;
+        if (!isfinite(v)) {
+          bad = true;
+          bad_m = min(bad_m, j0 + e % mb);
+        }
+      }
+    }
+    if (bad) l96_flag_divergence(st, step, bad_m);
+    __syncthreads();  // x ring complete; every thread is past stage 3's reads of sa
+  }
+#pragma unroll
+  for (int t = 0; t < PT; ++t)
+    if (gidx[t] >= 0) Xout[(int64_t)gidx[t]] = xr[t];
+}
+
 // Global-memory path, one RK4 stage per launch over all (i, j).
 //   s = 0: k1 from x;   acc = k1;          out = x + (dt/2) k1
 //   s = 1: k2 from in;  acc += 2 k2;       out = x + (dt/2) k2
