@@ -116,7 +116,7 @@ typedef struct enkf_plan_options {
   int32_t tiny_kernel;        /* 1: single-CTA step for desk-scale shapes (default), 0: multi-kernel */
   int32_t host_stream;        /* 1: streamed host entry (default), 0: copy in / step / copy out */
   int32_t host_trace;         /* 1: phase times of the host entry on stderr */
-  int64_t host_chunk_bytes;   /* X / XA chunk of the streamed host entry (default 256 MiB) */
+  int64_t host_chunk_bytes;   /* X / XA chunk of the streamed host entry (default 256 MiB; 0 = the smallest chunk) */
   int64_t host_ring_bytes;    /* pinned staging-ring slot for pageable buffers (default 256 MiB) */
   int64_t host_stream_min_bytes; /* pageable X from this size streams through the rings (default 1 GiB) */
 } enkf_plan_options;

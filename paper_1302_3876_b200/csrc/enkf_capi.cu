@@ -710,7 +710,7 @@ int32_t enkf_plan_create_ex(int64_t n_state, int64_t n_obs, int64_t n_ens, const
     if (options->struct_size != (int32_t)sizeof(enkf_plan_options) || options->gram_kernel < 0 ||
         options->gram_kernel > ENKF_GRAM_FP64 || options->anomaly_kernel < 0 ||
         options->anomaly_kernel > ENKF_ANOMALY_FP64 || options->levels_kernel < 0 ||
-        options->levels_kernel > ENKF_LEVELS_PER_LEVEL || options->host_chunk_bytes <= 0 ||
+        options->levels_kernel > ENKF_LEVELS_PER_LEVEL || options->host_chunk_bytes < 0 ||
         options->host_ring_bytes <= 0 || options->host_stream_min_bytes < 0) {
       set_status(st, ENKF_INVALID_ARGUMENT, "invalid enkf_plan_options (start from enkf_plan_options_default)");
       if (out) *out = nullptr;

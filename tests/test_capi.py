@@ -106,7 +106,7 @@ def test_plan_create_ex_rejects_bad_options(so):
     from enkf_plan_options_default, or an out-of-range kernel choice, is
     ENKF_INVALID_ARGUMENT with a null plan."""
     lib = _native.lib()
-    for field, value in (("struct_size", 8), ("gram_kernel", 7), ("levels_kernel", -1), ("host_chunk_bytes", 0)):
+    for field, value in (("struct_size", 8), ("gram_kernel", 7), ("levels_kernel", -1), ("host_chunk_bytes", -1)):
         o = _native.default_options()
         setattr(o, field, value)
         h, st = ctypes.c_void_p(), _native.EnkfStatus()
