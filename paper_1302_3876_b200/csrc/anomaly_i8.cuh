@@ -474,25 +474,37 @@ anomaly_i8_kernel(const double* __restrict__ X, const double* __restrict__ T,
         // slicer warp that formed these 8 rows flagged them
         static_assert(I8_TILE / I8_SLICE_WARPS == 8 && 8 % I8_RPT == 0, "epilogue rows within one slicer row group");
         const bool slow = rflag[(int)(it % (2 * I8_NBUF)) * I8_SLICE_WARPS + (r0 >> 3)] != 0;
+        // Instruction count matters here: the epilogue is ~45 % of the kernel's issued
+        // instructions, and under the board's power cap (SM clock ~1.3 GHz) issue slots
+        // bound the tile time.  sext(small) + d2 2^36 is formed directly as a register
+        // pair (high word (small >> 31) + 16 d2), then three mad.wide add d5 2^12,
+        // d4 2^20, d3 2^28: 8 integer instructions per output before the conversion.
         auto sprime = [&](int r) {
           const int d2 = (int)v[0][r], d3 = (int)v[1][r], d4 = (int)v[2][r], d5 = (int)v[3][r];
           const int d6 = (int)v[4][r], d7 = (int)v[5][r];
           int small = d6 * 16 + (d7 >> 4);  // |.| < 2^31
           if constexpr (I8_NLEV > 6) small += (int)v[I8_NLEV > 6 ? 6 : 0][r] >> 12;
-          long long sp = (long long)d5 * 4096 + (long long)small;
-          sp += (long long)d4 * 1048576;
-          sp += (long long)d3 * 268435456;
-          sp += (long long)((unsigned long long)(unsigned)(d2 * 16) << 32);  // d2 2^36: high word only
+          const int hi0 = (small >> 31) + d2 * 16;
+          long long sp = __double_as_longlong(__hiloint2double(hi0, small));  // register pair, no instruction
+          sp = (long long)d5 * 4096 + sp;
+          sp = (long long)d4 * 1048576 + sp;
+          sp = (long long)d3 * 268435456 + sp;
           return (double)sp;
         };
-        if (!slow) {
+        // scale by 2^k through the exponent field; an exact zero stays zero
+        auto scaled = [&](int r) {
+          const double dd = sprime(r);
+          int hi = __double2hiint(dd);
+          asm("{\n.reg .pred p;\nsetp.ne.s32 p, %0, 0;\n@p mad.lo.s32 %0, %1, 1048576, %0;\n}" : "+r"(hi) : "r"(kr[r]));
+          return __hiloint2double(hi, __double2loint(dd));
+        };
+        if (!slow && nvalid == I8_RPT) {
 #pragma unroll
-          for (int r = 0; r < I8_RPT; ++r) {
-            const double dd = sprime(r);
-            const int hi = __double2hiint(dd);
-            const double res = __hiloint2double(hi == 0 ? 0 : hi + (kr[r] << 20), __double2loint(dd));
-            if (r < nvalid) orow[r * I8_N] = res;
-          }
+          for (int r = 0; r < I8_RPT; ++r) orow[r * I8_N] = scaled(r);
+        } else if (!slow) {
+#pragma unroll
+          for (int r = 0; r < I8_RPT; ++r)
+            if (r < nvalid) orow[r * I8_N] = scaled(r);
         } else {
 #pragma unroll
           for (int r = 0; r < I8_RPT; ++r)
