@@ -202,21 +202,10 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
       xv[u][j] = valid[u] ? __ldcs(X + src[u] * G8_N + lane + 32 * j) : 0.0;
       yv[u][j] = valid[u] ? __ldcs(Y + (g0 + u) * G8_N + lane + 32 * j) : 0.0;
     }
-  // sqrt(1/r) of the warp's 4 rows: lane l evaluates row l & 3 (one pass through the
-  // FP64 divide and square root for all four rows instead of four warp-wide passes —
-  // ~55 instructions each, a quarter of this kernel's instruction count), then a
-  // broadcast per row.  Same operations on the same operands: bit-identical.
-  double sr_mine;
-  {
-    const int q = lane & 3;
-    const double rq = q == 0 ? rv[0] : q == 1 ? rv[1] : q == 2 ? rv[2] : rv[3];
-    sr_mine = g8_sqrt_rho(rq);
-  }
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const double mean = warp_sum((xv[u][0] + xv[u][1]) + (xv[u][2] + xv[u][3])) * (1.0 / G8_N);
-    const double sr_u = __shfl_sync(0xffffffffu, sr_mine, u);
-    const double sr = valid[u] ? sr_u : 0.0;
+    const double sr = valid[u] ? g8_sqrt_rho(rv[u]) : 0.0;
     unsigned long long* vrow = vals + (4 * warp + u) * G8_VLD;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
