@@ -490,10 +490,10 @@ def run_ours(args):
         step()
     runner.check(sptr)
     # Large configs: the library records its stage-boundary events during the timed
-    # steps themselves (5 cudaEventRecord per 9-45 ms step; each step overwrites the same
-    # events), so `kernels_ms` and the rooflines are the LAST TIMED step's stages, measured
-    # inside the timed region in its steady power state.  Small configs (tens of
-    # microseconds per step) keep the events out of the timed region.
+    # steps themselves (5 cudaEventRecord per 9-45 ms step, into a ring of 64 event sets),
+    # so `kernels_ms` and the rooflines are the MEAN over the timed steps (the last 64 at
+    # most), measured inside the timed region in its steady power state.  Small configs
+    # (tens of microseconds per step) keep the events out of the timed region.
     stage_in_region = not small
     if stage_in_region:
         runner.lib.enkf_debug_set_stage_events(runner.plan.handle, 1)
@@ -503,11 +503,16 @@ def run_ours(args):
     sync = lambda: torch.cuda.synchronize(dev)  # noqa: E731
 
     stages = None
+    stage_steps = 0
     if stage_in_region:
         import ctypes
         four = (ctypes.c_float * 4)()
-        if runner.lib.enkf_debug_stage_times(runner.plan.handle, four) == 0:
+        nst = ctypes.c_int32(0)
+        runner.lib.enkf_debug_stage_times_mean.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
+                                                           ctypes.POINTER(ctypes.c_int32)]
+        if runner.lib.enkf_debug_stage_times_mean(runner.plan.handle, four, ctypes.byref(nst)) == 0:
             stages = dict(zip(("gram", "allreduce", "levels", "anomaly"), (float(v) for v in four)))
+            stage_steps = int(nst.value)
         runner.lib.enkf_debug_set_stage_events(runner.plan.handle, 0)
     if stages is None:
         stage_in_region = False
@@ -752,7 +757,7 @@ def run_ours(args):
                    "l2": ("inputs larger than L2 (X is %.0f GiB per GPU)" % (ns_loc * n * 8 / 2**30)) if not small
                    else "inputs L2-resident (latency-bound configuration)"},
         "kernels_ms": stages,
-        "kernels_ms_source": ("library stage events of the last timed step (inside the timed region)"
+        "kernels_ms_source": (f"library stage events, mean over {stage_steps} timed steps (inside the timed region)"
                               if stage_in_region else
                               "library stage events of 3 extra steps after the timed region (averaged)"),
         "kernels_ms_per_rank": stages_all,

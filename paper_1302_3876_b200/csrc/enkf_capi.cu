@@ -102,7 +102,10 @@ struct enkf_plan {
   int nccl_rc = 0;
   // measurement: events at the stage boundaries of the analysis step
   bool stage_events = false;
-  cudaEvent_t st_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  static constexpr int ST_SETS = 64;  // stage-event sets: one per step, a ring (the last 64 steps are kept)
+  cudaEvent_t st_evs[ST_SETS][5] = {};
+  cudaEvent_t* st_ev = st_evs[0];     // the set the current step records into
+  long st_steps = 0;                  // steps recorded since the events were switched on
 };
 
 namespace {
@@ -878,8 +881,9 @@ void enkf_plan_destroy(enkf_plan* p) {
   cudaFree(p->g8_ls_partial);
   cudaFree(p->g8_ls_progress);
   cudaFree(p->cyc_status);
-  for (cudaEvent_t ev : p->st_ev)
-    if (ev) cudaEventDestroy(ev);
+  for (auto& set : p->st_evs)
+    for (cudaEvent_t ev : set)
+      if (ev) cudaEventDestroy(ev);
   for (int i = 0; i < 2; ++i) {
     if (p->ring[i]) cudaFreeHost(p->ring[i]);
     if (p->ring_ev[i]) cudaEventDestroy(p->ring_ev[i]);
@@ -929,8 +933,10 @@ int32_t enkf_analysis_async_f64(enkf_plan* p, const double* X, const double* Y, 
     return e == cudaSuccess ? ENKF_OK : ENKF_CUDA_ERROR;
   }
   if (p->stage_events) {
-    for (cudaEvent_t& ev : p->st_ev)
-      if (!ev && cudaEventCreate(&ev) != cudaSuccess) return ENKF_CUDA_ERROR;
+    p->st_ev = p->st_evs[p->st_steps % enkf_plan::ST_SETS];
+    ++p->st_steps;
+    for (int i = 0; i < 5; ++i)
+      if (!p->st_ev[i] && cudaEventCreate(&p->st_ev[i]) != cudaSuccess) return ENKF_CUDA_ERROR;
     cudaEventRecord(p->st_ev[0], s);
   }
   if (e == cudaSuccess) e = launch_gram_global(p, X, Y, idx, r, s);
@@ -1639,8 +1645,6 @@ int cycle_l96(enkf_plan* p, double* X, const double* Ys, const int64_t* idx, con
   cudaStream_t s = (cudaStream_t)stream;
   if (p->cyc_cap < n_cycles) {
     cudaFree(p->cyc_status);
-  for (cudaEvent_t ev : p->st_ev)
-    if (ev) cudaEventDestroy(ev);
     p->cyc_status = nullptr;
     p->cyc_cap = 0;
     CUDA_TRY(cudaMalloc(&p->cyc_status, sizeof(DevStatus) * (size_t)n_cycles), st);
@@ -1819,6 +1823,7 @@ int32_t enkf_plan_set_comm(enkf_plan* p, void* comm, enkf_status* st) {
 // boundaries of enkf_analysis_async_f64 (gram | allreduce | levels | anomaly).
 __attribute__((visibility("default"))) int32_t enkf_debug_set_stage_events(enkf_plan* p, int32_t on) {
   if (!p) return ENKF_INVALID_ARGUMENT;
+  if (on && !p->stage_events) p->st_steps = 0;  // a new measurement window
   p->stage_events = on != 0;
   return ENKF_OK;
 }
@@ -1827,6 +1832,24 @@ __attribute__((visibility("default"))) int32_t enkf_debug_stage_times(enkf_plan*
   if (!p || !p->st_ev[4]) return ENKF_INVALID_ARGUMENT;
   for (int i = 0; i < 4; ++i)
     if (cudaEventElapsedTime(&out4[i], p->st_ev[i], p->st_ev[i + 1]) != cudaSuccess) return ENKF_CUDA_ERROR;
+  return ENKF_OK;
+}
+// mean ms of the four stages over the steps recorded since the events were switched on
+// (at most the last 64; caller synchronised); *n_steps = how many were averaged
+__attribute__((visibility("default"))) int32_t enkf_debug_stage_times_mean(enkf_plan* p, float* out4, int32_t* n_steps) {
+  if (!p || p->st_steps <= 0) return ENKF_INVALID_ARGUMENT;
+  const long n = p->st_steps < enkf_plan::ST_SETS ? p->st_steps : (long)enkf_plan::ST_SETS;
+  double acc[4] = {0, 0, 0, 0};
+  for (long k = 0; k < n; ++k) {
+    cudaEvent_t* ev = p->st_evs[(p->st_steps - 1 - k) % enkf_plan::ST_SETS];
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      if (!ev[i] || !ev[i + 1] || cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) != cudaSuccess) return ENKF_CUDA_ERROR;
+      acc[i] += ms;
+    }
+  }
+  for (int i = 0; i < 4; ++i) out4[i] = (float)(acc[i] / (double)n);
+  if (n_steps) *n_steps = (int32_t)n;
   return ENKF_OK;
 }
 
