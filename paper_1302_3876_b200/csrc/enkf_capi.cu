@@ -45,6 +45,7 @@ struct enkf_plan {
   bool host_trace = false;      // ENKF_HOST_TRACE=1: phase times of the streamed host path on stderr
   bool gram_i8 = true;         // tensor-core (int8 digit) Gram, N == 128 analysis mode (ENKF_GRAM=fp64: DMMA)
   int g8_groups = 0;           // groups of 4 CTAs over the observation rows
+  double* g8_sr = nullptr;                // [n_obs] sqrt(1/r) of the call's observation rows
   double* g8_ls_partial = nullptr;        // [groups][4][256][128] (level-split form)
   int* g8_ls_progress = nullptr;          // [groups][4] blocks issued per CTA (level-split pacing)
   bool loc_dmma = true;                   // localized update on FP64 DMMA (ENKF_LOCALIZED=fma: CUDA-core form)
@@ -236,6 +237,8 @@ cudaError_t ensure_gram_i8_workspace(enkf_plan* p) {
   if (!p->g8_planes && n_blocks > 0 &&
       (e = cudaMalloc(&p->g8_planes, (size_t)n_blocks * G8_BLOCK_BYTES)) != cudaSuccess)
     return e;
+  if (!p->g8_sr && p->n_obs > 0 && (e = cudaMalloc(&p->g8_sr, sizeof(double) * (size_t)p->n_obs)) != cudaSuccess)
+    return e;
   if (!p->g8_ls_partial &&
       (e = cudaMalloc(&p->g8_ls_partial, sizeof(double) * (size_t)p->g8_groups * 4 * 2 * G8_N * G8_N)) != cudaSuccess)
     return e;
@@ -269,7 +272,9 @@ cudaError_t launch_gram_i8(enkf_plan* p, const double* X, const double* Y, const
     return e;
   // 2 CTAs per SM are resident (120 registers x 256 threads): one full wave, no tail
   const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)p->num_sms * G8_SLICE_CTAS_PER_SM);
-  gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, r, p->g8_meta, p->n_state,
+  gram_i8_sqrt_rho_kernel<<<(unsigned)std::min<int64_t>((p->n_obs + 255) / 256, (int64_t)p->num_sms * 8), 256, 0, s>>>(
+      r, p->n_obs, p->g8_sr, p->dstatus);
+  gram_i8_slice_kernel<<<(unsigned)grid, G8_SLICE_THREADS, smem, s>>>(X, Y, idx, p->g8_sr, p->g8_meta, p->n_state,
                                                                        p->n_obs, n_blocks, p->g8_planes, overflow,
                                                                        p->dstatus);
   if (p->g8_events) cudaEventRecord(p->g8_ev[1], s);
@@ -878,6 +883,7 @@ void enkf_plan_destroy(enkf_plan* p) {
   for (cudaEvent_t ev : p->g8_ev)
     if (ev) cudaEventDestroy(ev);
   cudaFree(p->g8_meta);
+  cudaFree(p->g8_sr);
   cudaFree(p->g8_ls_partial);
   cudaFree(p->g8_ls_progress);
   cudaFree(p->cyc_status);

@@ -151,6 +151,24 @@ __global__ void __launch_bounds__(256) gram_i8_scales_kernel(const double* __res
     if (red[e]) atomicMax(&cmax[e], red[e]);
 }
 
+// sqrt(1/r) of every observation row, once (thread per row), with the checks of r
+// (sherman.py:96-101: finite, positive).  The slice pass then loads the result instead
+// of evaluating the FP64 divide and square root in every warp for its 4 rows — a
+// quarter of that pass's instructions, which at the power-capped SM clock is what
+// bounds it.  Same function on the same input: bit-identical digits.
+__global__ void gram_i8_sqrt_rho_kernel(const double* __restrict__ r, int64_t n_obs, double* __restrict__ sr,
+                                        DevStatus* __restrict__ status) {
+  int flags = 0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_obs; g += (int64_t)gridDim.x * blockDim.x) {
+    const double rv = r[g];
+    if (!isfinite(rv)) flags |= FLAG_NONFINITE;
+    else if (!(rv > 0.0)) flags |= FLAG_R_NONPOS;
+    sr[g] = g8_sqrt_rho(rv);
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&status->flags, flags);
+}
+
 // ---------------------------------------------------------------------------
 // Slicing of one 32-row block by 8 warps (256 threads, slicer thread index st).
 // Phase 1 (warp w: rows 4w..4w+3 of the block, lane: members lane + 32j): the
@@ -162,12 +180,12 @@ __global__ void __launch_bounds__(256) gram_i8_scales_kernel(const double* __res
 // so vals can be reused).
 template <class Sync>
 __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, const double* __restrict__ Y,
-                                               const int64_t* __restrict__ idx, const double* __restrict__ r,
+                                               const int64_t* __restrict__ idx, const double* __restrict__ sqrt_rho,
                                                int64_t n_state, int64_t n_obs, int64_t blk, int st,
                                                const double (&sp)[4], const double (&sq)[4],
                                                unsigned long long* vals, unsigned char* __restrict__ out,
                                                int& flags, int& ovf, Sync sync) {
-  constexpr unsigned long long kBias = 0x808080808080ull;
+  const double kMagicB = 6755399441055744.0 + (double)0x808080808080ull;  // 1.5 2^52 + the digit bias
   const int lane = st & 31, warp = st >> 5;
   // ---- phase 1
   const int64_t g0 = blk * G8_KB + 4 * warp;
@@ -181,7 +199,7 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
     src[u] = g;
     rv[u] = 1.0;
     if (valid[u]) {
-      rv[u] = r[g];
+      rv[u] = sqrt_rho[g];  // sqrt(1/r[g]) (gram_i8_sqrt_rho_kernel, which also checked r)
       if (idx) {
         src[u] = idx[g];
         if (lane == 0 && g > 0 && idx[g - 1] >= src[u]) flags |= FLAG_IDX_ORDER;
@@ -190,8 +208,6 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
           valid[u] = false;
         }
       }
-      if (!isfinite(rv[u])) flags |= FLAG_NONFINITE;
-      else if (!(rv[u] > 0.0)) flags |= FLAG_R_NONPOS;
     }
   }
   double xv[4][4], yv[4][4];
@@ -205,22 +221,22 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const double mean = warp_sum((xv[u][0] + xv[u][1]) + (xv[u][2] + xv[u][3])) * (1.0 / G8_N);
-    const double sr = valid[u] ? g8_sqrt_rho(rv[u]) : 0.0;
+    const double sr = valid[u] ? rv[u] : 0.0;
     unsigned long long* vrow = vals + (4 * warp + u) * G8_VLD;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      // V = round(v 2^(47-e)): fma(v, sc, 1.5 2^52) holds V in its low 51 bits (the
-      // high word minus 0x43380000 is floor(V / 2^32)).  The six balanced digits
-      // represent V iff V + bias lies in [0, 2^48): anything else (|V| near or
-      // above 2^47, non-finite inputs) sets the overflow flag.
-      const double tp = fma(sr * (xv[u][j] - mean), sp[j], 6755399441055744.0);
-      const double tq = fma(sr * (yv[u][j] - xv[u][j]), sq[j], 6755399441055744.0);
-      const int hp = __double2hiint(tp) - 0x43380000, hq = __double2hiint(tq) - 0x43380000;
-      const unsigned long long bp = ((unsigned long long)(uint32_t)hp << 32 | (uint32_t)__double2loint(tp)) + kBias;
-      const unsigned long long bq = ((unsigned long long)(uint32_t)hq << 32 | (uint32_t)__double2loint(tq)) + kBias;
-      ovf |= ((uint32_t)(bp >> 32) >= 0x10000u) | ((uint32_t)(bq >> 32) >= 0x10000u);
-      vrow[lane + 32 * j] = bp;
-      vrow[G8_N + lane + 32 * j] = bq;
+      // V = round(v 2^(47-e)): fma(v, sc, 1.5 2^52 + bias) holds V + bias in the low 51
+      // bits of its mantissa (bias and 1.5 2^52 are even integers and the sum stays in
+      // [2^52, 2^53), so the rounding is the rounding of v sc alone): the low word is
+      // the low word of V + bias, the high word minus 0x43380000 its high word.  The six
+      // balanced digits represent V iff V + bias lies in [0, 2^48): anything else (|V|
+      // near or above 2^47, non-finite inputs) sets the overflow flag.
+      const double tp = fma(sr * (xv[u][j] - mean), sp[j], kMagicB);
+      const double tq = fma(sr * (yv[u][j] - xv[u][j]), sq[j], kMagicB);
+      const uint32_t hp = (uint32_t)__double2hiint(tp) - 0x43380000u, hq = (uint32_t)__double2hiint(tq) - 0x43380000u;
+      ovf |= (hp >= 0x10000u) | (hq >= 0x10000u);
+      vrow[lane + 32 * j] = (unsigned long long)hp << 32 | (uint32_t)__double2loint(tp);
+      vrow[G8_N + lane + 32 * j] = (unsigned long long)hq << 32 | (uint32_t)__double2loint(tq);
     }
   }
   sync();
@@ -268,7 +284,7 @@ __device__ __forceinline__ void g8_slice_block(const double* __restrict__ X, con
 #endif
 __global__ void __launch_bounds__(G8_SLICE_THREADS, G8_SLICE_MINB)
 gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y, const int64_t* __restrict__ idx,
-                     const double* __restrict__ r, const unsigned long long* __restrict__ cmax, int64_t n_state,
+                     const double* __restrict__ sqrt_rho, const unsigned long long* __restrict__ cmax, int64_t n_state,
                      int64_t n_obs, int64_t n_blocks, unsigned char* __restrict__ planes, int* __restrict__ overflow,
                      DevStatus* __restrict__ status) {
   extern __shared__ __align__(16) unsigned char g8s_raw[];
@@ -285,7 +301,7 @@ gram_i8_slice_kernel(const double* __restrict__ X, const double* __restrict__ Y,
   }
   int flags = 0, ovf = 0;
   for (int64_t blk = blockIdx.x; blk < n_blocks; blk += gridDim.x)
-    g8_slice_block(X, Y, idx, r, n_state, n_obs, blk, tid, sp, sq, vals, planes + (size_t)blk * G8_BLOCK_BYTES,
+    g8_slice_block(X, Y, idx, sqrt_rho, n_state, n_obs, blk, tid, sp, sq, vals, planes + (size_t)blk * G8_BLOCK_BYTES,
                    flags, ovf, [] { __syncthreads(); });
   flags = __reduce_or_sync(0xffffffffu, flags);
   ovf = __reduce_or_sync(0xffffffffu, ovf);
